@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""Benchmark of the docking hot path (BASELINE.json configs[1]).
+
+Workload (`cfg1-score-1M`): 1,000,000 random genotypes of one 40-atom /
+8-torsion synthetic ligand (seeded), scored against 80^3
+maps built on the GPU from a 4,000-atom synthetic receptor.  A step = one
+fused pose+inter+intra pass over the 1M genotypes (per rank: weak scaling).
+
+Arms
+  default            our CUDA path.  `value`: genes resident in HBM, CUDA
+                     events around each step's kernel, L2 flushed (256 MiB
+                     write) before every timed step; `e2e`: the public
+                     backend API with pinned host genes -> host results.
+  --impl reference   the reference's CPU algorithm (the bit-exact C port in
+                     oracle/, all host threads) on bounded samples of the
+                     same workload; rank 0 only.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "pose evaluations/sec"
+UNIT = "poses/s"
+N_POSES = 1_000_000
+WORKLOAD = "cfg1-score-1M"
+FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def build_inputs(device_grid: bool):
+    from paper_2509_12232_b200 import chem, context, gridmaps, synth
+
+    cfg = synth.CONFIGS[1]
+    spec = synth.config_grid_spec(1)
+    prot = synth.config_protein(1)
+    lig = synth.config_ligand(1, 0)
+    t0 = time.perf_counter()
+    if device_grid:
+        gset = gridmaps.build_grid_maps(prot, spec, cfg.probe_types)
+        grid_src = "device (vd_grid_build)"
+    else:
+        from oracle import oracle
+
+        w = chem.TermWeights()
+        maps = oracle.build_grid(prot, spec.origin, spec.spacing, spec.dims, cfg.probe_types, w,
+                                 chem.default_parameter_table(), n_threads=0)
+        labels = list(cfg.probe_types) + [chem.ELEC_LABEL, chem.DESOLV_LABEL]
+        gset = gridmaps.GridMapSet(spec, {l: maps[k] for k, l in enumerate(labels)})
+        grid_src = "host (oracle C builder)"
+    grid_s = time.perf_counter() - t0
+    ctx = context.prepare_context(lig, gset)
+    return gset, lig, ctx, grid_s, grid_src
+
+
+def flops_per_pose(ctx):
+    # the reference's own model (vd/bench.py:139-171): 32 flops/pair + 107 flops/atom
+    return 32 * ctx.n_pairs + 107 * ctx.n_atoms
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def smi_index(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    ids = [v for v in vis.split(",") if v.strip()]
+    if ids and all(v.strip().isdigit() for v in ids) and local_rank < len(ids):
+        return int(ids[local_rank])
+    return local_rank
+
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2509_12232_b200 import _abi, synth
+    from paper_2509_12232_b200.backend import CudaBackend
+
+    _abi.ensure_device(local)
+    gset, lig, ctx, grid_s, grid_src = build_inputs(device_grid=True)
+    spec = gset.spec
+    b = CudaBackend(mode="fast", device=local)
+    grid, ligs = b.prepared(ctx)
+    genes_h = synth.random_genes(rank, N_POSES, ctx.n_torsions, spec.origin, spec.upper)
+    dev = torch.device("cuda", local)
+    genes_d = torch.from_numpy(genes_h).to(dev)
+    out_d = (torch.empty(N_POSES, dtype=torch.float64, device=dev),
+             torch.empty(N_POSES, dtype=torch.float64, device=dev),
+             torch.empty(N_POSES, dtype=torch.float32, device=dev))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def step():
+        _abi.score_genes(grid, ligs, 0, genes_d, *out_d, mode=_abi.MODE_FAST, stream=sp)
+
+    for _ in range(args.warmup):
+        flush.fill_(1)
+        step()
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    l0 = _abi.launches()
+    with ClockSampler(smi_index(local)) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xFF)
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        # keep the GPU busy a little longer so the sampler sees a loaded clock
+        if clk.proc and len(clk.rows) < 3:
+            t_end = time.time() + 0.5
+            while time.time() < t_end:
+                step()
+            torch.cuda.synchronize(dev)
+    launches = _abi.launches() - l0
+    ms = [a.elapsed_time(z) for a, z in evs]
+    t_loc = sum(ms) / 1e3
+    t_max = t_loc
+    if dist:
+        tt = torch.tensor([t_loc], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+    value = world * N_POSES * args.steps / t_max
+    ms_per_step = 1e3 * t_max / args.steps
+
+    # sanity: device results agree with the oracle on a sample (not timed)
+    from oracle import oracle
+
+    sub = slice(0, N_POSES, 997)
+    _, _, wt = oracle.dock_population(oracle.Ligand(ctx), genes_h[sub], n_threads=0)
+    got_t = out_d[2].cpu().numpy()[sub]
+    d = np.abs(got_t.astype(np.float64) - wt)
+    parity_ok = bool(np.all((d <= 1e-3) | (d <= 1e-4 * np.abs(wt))))
+
+    # e2e: public API, pinned host genes in, host results out, copies inside the region
+    pin_g = torch.from_numpy(genes_h).pin_memory()
+    pin_out = (torch.empty(N_POSES, dtype=torch.float64).pin_memory(),
+               torch.empty(N_POSES, dtype=torch.float64).pin_memory(),
+               torch.empty(N_POSES, dtype=torch.float32).pin_memory())
+    outs_np = tuple(t.numpy() for t in pin_out)
+    g_np = pin_g.numpy()
+    for _ in range(2):
+        b.score_population_arrays(g_np, ctx, out=outs_np)
+    e2e_steps = max(3, min(args.steps, 20))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        b.score_population_arrays(g_np, ctx, out=outs_np)
+    torch.cuda.synchronize(dev)
+    te = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+    e2e_value = world * N_POSES * e2e_steps / te
+
+    fpp = flops_per_pose(ctx)
+    achieved = fpp * N_POSES / (t_loc / args.steps) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (pose stage f32/f64 bit-exact)",
+        "data": "synthetic (SURVEY Appendix B recipes, seeded)",
+        "config": {"workload": WORKLOAD, "poses_per_step_per_gpu": N_POSES,
+                   "ligand_atoms": int(ctx.n_atoms), "torsions": int(ctx.n_torsions),
+                   "pairs": int(ctx.n_pairs), "grid": "80^3 x 9 maps @0.375A",
+                   "receptor_atoms": 4000, "mode": "fast",
+                   "l2": "flushed (256 MiB write) before every timed step",
+                   "parallelism": f"ligand/pose sharding x{world}, no data-path collective",
+                   "grid_build_s": round(grid_s, 4), "grid_built_on": grid_src},
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": int(genes_h.nbytes),
+                "d2h_bytes_per_step": int(N_POSES * (8 + 8 + 4)),
+                "path": "CudaBackend.score_population_arrays (pinned numpy in/out)"},
+        "roofline": {"bound": "fp32", "achieved": achieved, "peak": FP32_SPEC_TFLOPS,
+                     "unit": "TFLOP/s", "frac": achieved / FP32_SPEC_TFLOPS, "traffic": None,
+                     "kernel": "vd::score_kernel<false,128,0>",
+                     "algorithmic_flops_per_pose": fpp,
+                     "peak_source": "spec-derived 2*128 lanes*148 SMs*1.965 GHz (no measured "
+                                    "FP32 figure in MEASURED_PEAKS.json)"},
+        "gpu_launches": int(launches),
+        "parity_sample_ok": parity_ok,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(ctx, genes_h, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(ctx, genes, seconds=10.0):
+    from oracle import oracle
+
+    lig = oracle.Ligand(ctx)
+    cores = oracle.cores()
+    n = 4096
+    t0 = time.perf_counter()
+    oracle.dock_population(lig, genes[:n], n_threads=cores)
+    dt = time.perf_counter() - t0
+    n = int(min(len(genes), max(n, n * seconds / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.dock_population(lig, genes[:n], n_threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"first {n} of the {N_POSES} cfg1 genotypes, {dt:.1f} s on {cores} threads "
+                      "(oracle/vd_oracle.c, bit-exact restatement of SimdBackend.dock_population)"}
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return
+    from oracle import oracle
+    from paper_2509_12232_b200 import synth
+
+    gset, lig, ctx, grid_s, grid_src = build_inputs(device_grid=False)
+    spec = gset.spec
+    per_step = args.ref_sample
+    genes = synth.random_genes(0, per_step * 4, ctx.n_torsions, spec.origin, spec.upper)
+    L = oracle.Ligand(ctx)
+    cores = oracle.cores()
+    for k in range(args.warmup):
+        oracle.dock_population(L, genes[(k % 4) * per_step:((k % 4) + 1) * per_step], n_threads=cores)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        oracle.dock_population(L, genes[(k % 4) * per_step:((k % 4) + 1) * per_step], n_threads=cores)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (SURVEY Appendix B recipes, seeded)",
+        "config": {"workload": WORKLOAD, "poses_per_step": per_step, "grid_build_s": round(grid_s, 2),
+                   "grid_built_on": grid_src},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{per_step} cfg1 genotypes per step (of the 1M workload); "
+                                   "oracle/vd_oracle.c is bit-exact with the reference's simd "
+                                   "backend (tests/test_oracle_golden.py)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-sample", type=int, default=16384)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/*
+ * vecdock_b200.h -- C-ABI of the B200 docking hot path (libvdb200.so).
+ *
+ * Plain C types only.  Every entry returns 0 on success and < 0 on error,
+ * with a thread-local message in vd_last_error().  Pointers passed for bulk
+ * inputs/outputs may be host memory (pageable or pinned) or device memory
+ * (e.g. torch tensors' data_ptr()); the library detects which.  A call with
+ * any host output synchronises its stream before returning; an all-device
+ * call is asynchronous on `stream` (NULL = legacy default stream).
+ *
+ * Each entry replaces one reference seam (paths under
+ * /root/reference/pkg/src/vecdock):
+ *
+ *   vd_grid_create / vd_grid_build    grids.py:83-119 GridMapSet, grids.py:122-202
+ *                                     build_grid_maps; the map stack of
+ *                                     scoring/__init__.py:158-161 becomes one
+ *                                     shared device copy indexed per atom
+ *   vd_ligands_create                 scoring/__init__.py:133-207 prepare_context
+ *                                     (ScoringContext fields, CSR over ligands)
+ *   vd_score_genes                    SimdBackend.dock_population
+ *                                     (scoring/simd.py:294-311) + the total32
+ *                                     rounding of scoring/__init__.py:345
+ *   vd_score_poses                    SimdBackend.score_many (scoring/simd.py:277-292),
+ *                                     inter_one/intra_one with P = 1 (:250-275)
+ *   vd_pose_genes                     pose.pose_population (pose.py:137-205)
+ *   vd_dock_batch                     ga.dock (ga.py:180-235) for every ligand of a
+ *                                     screen_batch (screening.py:165-244), GA on device
+ */
+#ifndef VECDOCK_B200_H
+#define VECDOCK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VD_ABI_VERSION 1
+
+typedef struct vd_grid vd_grid;
+typedef struct vd_ligands vd_ligands;
+
+/* numerics of the energy stage (the pose stage is always bit-exact) */
+enum vd_mode {
+    VD_MODE_FAST = 0,  /* fp32 MUFU/FMA pair & lerp math, fp32 partials -> fp64 sums */
+    VD_MODE_EXACT = 1  /* the reference's canonical f32/f64 sequences and fp64
+                          summation order (scoring/reference.py:11-35, simd lane 8) */
+};
+
+int vd_abi_version(void);
+const char *vd_last_error(void);
+int vd_device_count(int *count);
+int vd_init(int device); /* select `device` for the calling thread, create its context */
+
+/* ---- grid maps (shared, read-only constant data) ------------------------ */
+/* maps: (n_maps, nx, ny, nz) f32, C order (z fastest), host or device. */
+int vd_grid_create(const float *maps, int n_maps, int nx, int ny, int nz, const float lo[3],
+                   const float hi[3], float spacing, vd_grid **out);
+
+typedef struct {
+    double r_eq, eps, volume, solpar;
+    int32_t donor, acceptor;
+} vd_atom_type;
+
+typedef struct {
+    double vdw, hbond, elec, desolv;
+} vd_weights;
+
+/* AutoGrid-style build on the device: probe maps (in `probe` order), then
+ * @elec, then @desolv; fp64 per-node sums over receptor atoms in order. */
+int vd_grid_build(const float *rec_xyz /* (3, n_rec) */, const int32_t *rec_type,
+                  const float *rec_charge, int n_rec, const vd_atom_type *table, int n_types,
+                  const int32_t *probe, int n_probe, const double origin[3], double spacing,
+                  int nx, int ny, int nz, const vd_weights *w, double cutoff, vd_grid **out);
+int vd_grid_n_maps(const vd_grid *g);
+int vd_grid_download(const vd_grid *g, float *out /* (n_maps, nx, ny, nz) host */);
+int vd_grid_destroy(vd_grid *g);
+
+/* ---- ligand set (ScoringContext records, CSR over L ligands) ------------- */
+typedef struct {
+    int32_t n_ligands;
+    const int32_t *atom_start;   /* [L+1] */
+    const int32_t *pair_start;   /* [L+1] */
+    const int32_t *tors_start;   /* [L+1] */
+    const float *centered0;      /* [sumN][3] pose_centered0, atom-major */
+    const float *charge;         /* [sumN] */
+    const float *desolv_factor;  /* [sumN] */
+    const int32_t *atom_map;     /* [sumN] grid map index of each atom's type map */
+    const int32_t *pair_i;       /* [sumP] ligand-local atom indices */
+    const int32_t *pair_j;
+    const float *pair_a, *pair_b, *pair_qq, *pair_desolv; /* [sumP] weight-folded */
+    const uint8_t *pair_hb;      /* [sumP] 12-10 flag */
+    const int32_t *axis_a;       /* [sumT] ligand-local */
+    const int32_t *axis_b;
+    const int32_t *frag_lo;      /* [sumT] absolute offsets into frag_index */
+    const int32_t *frag_hi;
+    const int32_t *frag_index;   /* [sumF] ligand-local atom indices */
+    const float *torsional32;    /* [L] f32(w_tors * T) */
+    const float *intra_cutoff2;  /* [L] (inf = none) */
+    const float *penalty_scale;  /* [L] out-of-box penalty (1e4) */
+    int32_t elec_map, desolv_map;
+} vd_ligand_arrays;
+
+int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out);
+int vd_ligands_n_torsions(const vd_ligands *s, int lig);
+int vd_ligands_destroy(vd_ligands *s);
+
+/* ---- scoring ------------------------------------------------------------ */
+/* genes: (P, 7 + T) f64 row-major; inter/intra f64 [P]; total f32 [P] (nullable). */
+int vd_score_genes(const vd_grid *g, const vd_ligands *s, int lig, const double *genes,
+                   int64_t P, double *inter, double *intra, float *total, int mode,
+                   void *stream);
+/* poses: (P, 3, N) f32. */
+int vd_score_poses(const vd_grid *g, const vd_ligands *s, int lig, const float *poses,
+                   int64_t P, double *inter, double *intra, int mode, void *stream);
+int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P,
+                  float *poses /* (P, 3, N) */, void *stream);
+
+/* ---- GA docking on device ------------------------------------------------ */
+typedef struct {
+    int32_t pop, generations, tournament, elitism;
+    double cx_rate, mut_rate, sigma_t, sigma_r, sigma_tor;
+    double lo[3], hi[3]; /* translation bounds (the grid box) */
+} vd_ga_params;
+
+/* Dock ligands [first, first + count) of the set; ligand l uses Philox key
+ * (seed, lig_index_base + l).  Outputs are indexed by l - first. */
+int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, int count,
+                  const vd_ga_params *p, uint64_t seed, int64_t lig_index_base, int mode,
+                  float *best_total, double *best_inter, double *best_intra,
+                  double *best_genes /* [count][gstride] */, int gstride,
+                  float *trace /* nullable [count][generations + 1] */, int64_t *n_evals,
+                  void *stream);
+
+/* device-side counters of the last call on this thread (kernel launches) */
+int vd_last_launch_count(int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VECDOCK_B200_H */

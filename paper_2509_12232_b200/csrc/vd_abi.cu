@@ -1,0 +1,442 @@
+/*
+ * vd_abi.cu -- the extern "C" boundary of libvdb200.so (see include/vecdock_b200.h).
+ *
+ * Handles own device memory; bulk arguments may be host or device pointers.
+ * Host-resident genotype batches are streamed through a two-stream chunk
+ * pipeline (H2D copy of chunk c+1 and D2H of chunk c-1 overlap the kernel on
+ * chunk c), which is what the e2e bench line measures.
+ */
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "vd_internal.h"
+
+namespace vd {
+cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
+                         const double *genes, const float *poses, int64_t P, int ngenes,
+                         double *inter, double *intra, float *total, cudaStream_t st);
+cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ngenes, float *out,
+                        cudaStream_t st);
+}  // namespace vd
+
+namespace vdi {
+static thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+bool check(cudaError_t e, const char *what)
+{
+    if (e == cudaSuccess) return true;
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    cudaGetLastError();
+    return false;
+}
+
+bool is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+vd::GridView grid_view(const vd_grid *g)
+{
+    vd::GridView v;
+    v.maps = g->d_maps;
+    v.nx = g->nx;
+    v.ny = g->ny;
+    v.nz = g->nz;
+    v.mstride = (int64_t)g->nx * g->ny * g->nz;
+    v.lo0 = g->lo[0]; v.lo1 = g->lo[1]; v.lo2 = g->lo[2];
+    v.hi0 = g->hi[0]; v.hi1 = g->hi[1]; v.hi2 = g->hi[2];
+    v.spacing = g->spacing;
+    return v;
+}
+
+/* Poses per CTA: the [3][N][B] f32 coordinate tile must fit in shared memory. */
+int pick_block(int n_atoms, int *block)
+{
+    const size_t limit = 200 * 1024;
+    for (int b : {128, 64, 32})
+        if ((size_t)12 * n_atoms * b <= limit) {
+            *block = b;
+            return 0;
+        }
+    set_error("ligand too large for the shared-memory pose tile (n_atoms = " +
+              std::to_string(n_atoms) + ")");
+    return -1;
+}
+
+struct Pipe {
+    cudaStream_t s[2];
+    cudaEvent_t start, done[2];
+};
+
+static Pipe *pipe_for_device()
+{
+    static thread_local std::map<int, Pipe> pipes;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = pipes.find(dev);
+    if (it != pipes.end()) return &it->second;
+    Pipe p;
+    for (int k = 0; k < 2; ++k) {
+        cudaStreamCreateWithFlags(&p.s[k], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&p.done[k], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
+    return &(pipes[dev] = p);
+}
+}  // namespace vdi
+
+vd::LigView vd_ligands::view(int l) const
+{
+    vd::LigView v;
+    const int a0 = atom_start[l], p0 = pair_start[l], t0 = tors_start[l];
+    v.n_atoms = atom_start[l + 1] - a0;
+    v.n_pairs = pair_start[l + 1] - p0;
+    v.n_torsions = tors_start[l + 1] - t0;
+    v.atom = d_atom + a0;
+    v.atom2 = d_atom2 + a0;
+    v.pij = d_pij + p0;
+    v.pcoef = d_pcoef + p0;
+    v.tors = d_tors + t0;
+    v.frag = d_frag;
+    v.tors32 = tors32[l];
+    v.cut2 = cut2[l];
+    v.penalty = penalty[l];
+    v.elec_map = elec_map;
+    v.desolv_map = desolv_map;
+    return v;
+}
+
+using vdi::set_error;
+
+extern "C" {
+
+int vd_abi_version(void) { return VD_ABI_VERSION; }
+const char *vd_last_error(void) { return vdi::g_err.c_str(); }
+
+int vd_last_launch_count(int64_t *launches)
+{
+    *launches = vdi::g_launches;
+    return 0;
+}
+
+int vd_device_count(int *count)
+{
+    *count = 0;
+    VD_CK(cudaGetDeviceCount(count));
+    return 0;
+}
+
+int vd_init(int device)
+{
+    VD_CK(cudaSetDevice(device));
+    VD_CK(cudaFree(0));
+    return 0;
+}
+
+int vd_grid_create(const float *maps, int n_maps, int nx, int ny, int nz, const float lo[3],
+                   const float hi[3], float spacing, vd_grid **out)
+{
+    *out = nullptr;
+    if (n_maps < 1 || nx < 2 || ny < 2 || nz < 2 || !(spacing > 0.f)) {
+        set_error("vd_grid_create: bad grid shape");
+        return -1;
+    }
+    const size_t n = (size_t)n_maps * nx * ny * nz;
+    if (n >= ((size_t)1 << 31)) {
+        set_error("vd_grid_create: map stack exceeds 2^31 values");
+        return -1;
+    }
+    vd_grid *g = new vd_grid();
+    cudaGetDevice(&g->device);
+    g->n_maps = n_maps;
+    g->nx = nx; g->ny = ny; g->nz = nz;
+    for (int k = 0; k < 3; ++k) { g->lo[k] = lo[k]; g->hi[k] = hi[k]; }
+    g->spacing = spacing;
+    if (!vdi::check(cudaMalloc(&g->d_maps, n * sizeof(float)), "cudaMalloc(maps)")) {
+        delete g;
+        return -1;
+    }
+    if (maps &&
+        !vdi::check(cudaMemcpy(g->d_maps, maps, n * sizeof(float), cudaMemcpyDefault), "upload maps")) {
+        cudaFree(g->d_maps);
+        delete g;
+        return -1;
+    }
+    *out = g;
+    return 0;
+}
+
+int vd_grid_n_maps(const vd_grid *g) { return g ? g->n_maps : -1; }
+
+int vd_grid_download(const vd_grid *g, float *out)
+{
+    const size_t n = (size_t)g->n_maps * g->nx * g->ny * g->nz;
+    VD_CK(cudaMemcpy(out, g->d_maps, n * sizeof(float), cudaMemcpyDefault));
+    return 0;
+}
+
+int vd_grid_destroy(vd_grid *g)
+{
+    if (!g) return 0;
+    cudaFree(g->d_maps);
+    delete g;
+    return 0;
+}
+
+int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
+{
+    *out = nullptr;
+    const int L = a->n_ligands;
+    if (L < 1) {
+        set_error("vd_ligands_create: need at least one ligand");
+        return -1;
+    }
+    const int NA = a->atom_start[L], NP = a->pair_start[L], NT = a->tors_start[L];
+    int NF = 0;
+    for (int t = 0; t < NT; ++t) NF = std::max(NF, a->frag_hi[t]);
+    std::vector<float4> atom(std::max(NA, 1));
+    std::vector<float2> atom2(std::max(NA, 1));
+    std::vector<uint32_t> pij(std::max(NP, 1));
+    std::vector<float4> pcoef(std::max(NP, 1));
+    std::vector<int4> tors(std::max(NT, 1));
+    std::vector<int> frag(std::max(NF, 1));
+    auto *s = new vd_ligands();
+    cudaGetDevice(&s->device);
+    s->n_ligands = L;
+    s->atom_start.assign(a->atom_start, a->atom_start + L + 1);
+    s->pair_start.assign(a->pair_start, a->pair_start + L + 1);
+    s->tors_start.assign(a->tors_start, a->tors_start + L + 1);
+    s->elec_map = a->elec_map;
+    s->desolv_map = a->desolv_map;
+    s->max_atoms = s->max_torsions = 0;
+    for (int l = 0; l < L; ++l) {
+        const int a0 = a->atom_start[l], n = a->atom_start[l + 1] - a0;
+        const int t0 = a->tors_start[l], T = a->tors_start[l + 1] - t0;
+        if (n < 1 || n > 32767) {
+            set_error("vd_ligands_create: ligand " + std::to_string(l) + " has " +
+                      std::to_string(n) + " atoms (need 1..32767)");
+            delete s;
+            return -1;
+        }
+        s->max_atoms = std::max(s->max_atoms, n);
+        s->max_torsions = std::max(s->max_torsions, T);
+        s->tors32.push_back(a->torsional32 ? a->torsional32[l] : 0.f);
+        s->cut2.push_back(a->intra_cutoff2 ? a->intra_cutoff2[l] : INFINITY);
+        s->penalty.push_back(a->penalty_scale ? a->penalty_scale[l] : 1.0e4f);
+        for (int i = 0; i < n; ++i) {
+            const int g = a0 + i;
+            atom[g] = make_float4(a->centered0[3 * g], a->centered0[3 * g + 1],
+                                  a->centered0[3 * g + 2], a->charge[g]);
+            int m = a->atom_map[g];
+            float mf;
+            std::memcpy(&mf, &m, sizeof mf);
+            atom2[g] = make_float2(a->desolv_factor[g], mf);
+        }
+        for (int k = a->pair_start[l]; k < a->pair_start[l + 1]; ++k) {
+            const int i = a->pair_i[k], j = a->pair_j[k];
+            if (i < 0 || j < 0 || i >= n || j >= n) {
+                set_error("vd_ligands_create: pair atom index out of range");
+                delete s;
+                return -1;
+            }
+            pij[k] = (uint32_t)i | ((uint32_t)j << 15) | ((a->pair_hb[k] ? 1u : 0u) << 31);
+            pcoef[k] = make_float4(a->pair_a[k], a->pair_b[k], a->pair_qq[k], a->pair_desolv[k]);
+        }
+        for (int t = t0; t < t0 + T; ++t) {
+            if (a->axis_a[t] < 0 || a->axis_a[t] >= n || a->axis_b[t] < 0 || a->axis_b[t] >= n ||
+                a->frag_lo[t] < 0 || a->frag_hi[t] < a->frag_lo[t]) {
+                set_error("vd_ligands_create: bad torsion record");
+                delete s;
+                return -1;
+            }
+            tors[t] = make_int4(a->axis_a[t], a->axis_b[t], a->frag_lo[t], a->frag_hi[t]);
+            for (int f = a->frag_lo[t]; f < a->frag_hi[t]; ++f) {
+                if (a->frag_index[f] < 0 || a->frag_index[f] >= n) {
+                    set_error("vd_ligands_create: fragment atom index out of range");
+                    delete s;
+                    return -1;
+                }
+                frag[f] = a->frag_index[f];
+            }
+        }
+    }
+    bool ok = vdi::check(cudaMalloc(&s->d_atom, atom.size() * sizeof(float4)), "alloc atoms") &&
+              vdi::check(cudaMalloc(&s->d_atom2, atom2.size() * sizeof(float2)), "alloc atoms2") &&
+              vdi::check(cudaMalloc(&s->d_pij, pij.size() * sizeof(uint32_t)), "alloc pairs") &&
+              vdi::check(cudaMalloc(&s->d_pcoef, pcoef.size() * sizeof(float4)), "alloc coef") &&
+              vdi::check(cudaMalloc(&s->d_tors, tors.size() * sizeof(int4)), "alloc tors") &&
+              vdi::check(cudaMalloc(&s->d_frag, frag.size() * sizeof(int)), "alloc frag") &&
+              vdi::check(cudaMemcpy(s->d_atom, atom.data(), atom.size() * sizeof(float4), cudaMemcpyHostToDevice), "up atoms") &&
+              vdi::check(cudaMemcpy(s->d_atom2, atom2.data(), atom2.size() * sizeof(float2), cudaMemcpyHostToDevice), "up atoms2") &&
+              vdi::check(cudaMemcpy(s->d_pij, pij.data(), pij.size() * sizeof(uint32_t), cudaMemcpyHostToDevice), "up pairs") &&
+              vdi::check(cudaMemcpy(s->d_pcoef, pcoef.data(), pcoef.size() * sizeof(float4), cudaMemcpyHostToDevice), "up coef") &&
+              vdi::check(cudaMemcpy(s->d_tors, tors.data(), tors.size() * sizeof(int4), cudaMemcpyHostToDevice), "up tors") &&
+              vdi::check(cudaMemcpy(s->d_frag, frag.data(), frag.size() * sizeof(int), cudaMemcpyHostToDevice), "up frag");
+    if (!ok) {
+        vd_ligands_destroy(s);
+        return -1;
+    }
+    *out = s;
+    return 0;
+}
+
+int vd_ligands_n_torsions(const vd_ligands *s, int lig)
+{
+    if (!s || lig < 0 || lig >= s->n_ligands) return -1;
+    return s->tors_start[lig + 1] - s->tors_start[lig];
+}
+
+int vd_ligands_destroy(vd_ligands *s)
+{
+    if (!s) return 0;
+    cudaFree(s->d_atom);
+    cudaFree(s->d_atom2);
+    cudaFree(s->d_pij);
+    cudaFree(s->d_pcoef);
+    cudaFree(s->d_tors);
+    cudaFree(s->d_frag);
+    delete s;
+    return 0;
+}
+
+/* Shared driver of vd_score_genes / vd_score_poses. */
+static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const void *in,
+                        bool in_is_genes, int64_t P, double *inter, double *intra, float *total,
+                        int mode, void *stream)
+{
+    if (!g || !s || lig < 0 || lig >= s->n_ligands) {
+        set_error("vd_score: bad grid/ligand handle or index");
+        return -1;
+    }
+    if (P <= 0) return 0;
+    if (!in || !inter || !intra) {
+        set_error("vd_score: null input/output");
+        return -1;
+    }
+    const vd::LigView L = s->view(lig);
+    const vd::GridView G = vdi::grid_view(g);
+    const int ngenes = 7 + L.n_torsions;
+    const size_t in_row = in_is_genes ? sizeof(double) * ngenes : sizeof(float) * 3 * L.n_atoms;
+    const int src = in_is_genes ? 0 : 1;
+    cudaStream_t cs = (cudaStream_t)stream;
+    const bool in_dev = vdi::is_device_ptr(in);
+    const bool oe = vdi::is_device_ptr(inter), oa = vdi::is_device_ptr(intra),
+               ot = total ? vdi::is_device_ptr(total) : true;
+    if (in_dev && oe && oa && ot) {
+        VD_CK(vd::launch_score(mode, src, G, L, in_is_genes ? (const double *)in : nullptr,
+                               in_is_genes ? nullptr : (const float *)in, P, ngenes, inter, intra,
+                               total, cs));
+        return 0;
+    }
+    /* chunked two-stream pipeline through device staging buffers */
+    vdi::Pipe *pp = vdi::pipe_for_device();
+    const int64_t CH = std::min<int64_t>(P, 1 << 17);
+    char *d_in[2] = {nullptr, nullptr};
+    double *d_e[2] = {nullptr, nullptr}, *d_a[2] = {nullptr, nullptr};
+    float *d_t[2] = {nullptr, nullptr};
+    VD_CK(cudaEventRecord(pp->start, cs));
+    int rc = 0;
+    for (int k = 0; k < 2 && rc == 0; ++k) {
+        cudaStream_t st = pp->s[k];
+        if (!vdi::check(cudaStreamWaitEvent(st, pp->start, 0), "wait") ||
+            (!in_dev && !vdi::check(cudaMallocAsync((void **)&d_in[k], CH * in_row, st), "alloc in")) ||
+            (!oe && !vdi::check(cudaMallocAsync((void **)&d_e[k], CH * sizeof(double), st), "alloc e")) ||
+            (!oa && !vdi::check(cudaMallocAsync((void **)&d_a[k], CH * sizeof(double), st), "alloc a")) ||
+            (total && !ot && !vdi::check(cudaMallocAsync((void **)&d_t[k], CH * sizeof(float), st), "alloc t")))
+            rc = -1;
+    }
+    for (int64_t off = 0, c = 0; off < P && rc == 0; off += CH, ++c) {
+        const int k = (int)(c & 1);
+        cudaStream_t st = pp->s[k];
+        const int64_t n = std::min(CH, P - off);
+        const char *src_in = (const char *)in + off * in_row;
+        const void *kin = src_in;
+        if (!in_dev) {
+            if (!vdi::check(cudaMemcpyAsync(d_in[k], src_in, n * in_row, cudaMemcpyHostToDevice, st), "H2D")) { rc = -1; break; }
+            kin = d_in[k];
+        }
+        double *ke = oe ? inter + off : d_e[k];
+        double *ka = oa ? intra + off : d_a[k];
+        float *kt = total ? (ot ? total + off : d_t[k]) : nullptr;
+        if (!vdi::check(vd::launch_score(mode, src, G, L, in_is_genes ? (const double *)kin : nullptr,
+                                         in_is_genes ? nullptr : (const float *)kin, n, ngenes, ke, ka, kt, st),
+                        "score kernel")) { rc = -1; break; }
+        if ((!oe && !vdi::check(cudaMemcpyAsync(inter + off, ke, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H e")) ||
+            (!oa && !vdi::check(cudaMemcpyAsync(intra + off, ka, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H a")) ||
+            (total && !ot && !vdi::check(cudaMemcpyAsync(total + off, kt, n * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H t")))
+            rc = -1;
+    }
+    for (int k = 0; k < 2; ++k) {
+        cudaStream_t st = pp->s[k];
+        if (d_in[k]) cudaFreeAsync(d_in[k], st);
+        if (d_e[k]) cudaFreeAsync(d_e[k], st);
+        if (d_a[k]) cudaFreeAsync(d_a[k], st);
+        if (d_t[k]) cudaFreeAsync(d_t[k], st);
+        cudaEventRecord(pp->done[k], st);
+        cudaStreamWaitEvent(cs, pp->done[k], 0);
+    }
+    if (rc) return rc;
+    if (!(oe && oa && ot)) {
+        VD_CK(cudaStreamSynchronize(pp->s[0]));
+        VD_CK(cudaStreamSynchronize(pp->s[1]));
+    }
+    return 0;
+}
+
+int vd_score_genes(const vd_grid *g, const vd_ligands *s, int lig, const double *genes,
+                   int64_t P, double *inter, double *intra, float *total, int mode, void *stream)
+{
+    return score_common(g, s, lig, genes, true, P, inter, intra, total, mode, stream);
+}
+
+int vd_score_poses(const vd_grid *g, const vd_ligands *s, int lig, const float *poses,
+                   int64_t P, double *inter, double *intra, int mode, void *stream)
+{
+    return score_common(g, s, lig, poses, false, P, inter, intra, nullptr, mode, stream);
+}
+
+int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, float *poses,
+                  void *stream)
+{
+    if (!s || lig < 0 || lig >= s->n_ligands) {
+        set_error("vd_pose_genes: bad ligand handle or index");
+        return -1;
+    }
+    if (P <= 0) return 0;
+    const vd::LigView L = s->view(lig);
+    const int ngenes = 7 + L.n_torsions;
+    cudaStream_t st = (cudaStream_t)stream;
+    const double *dg = genes;
+    float *dp = poses;
+    const bool gin = vdi::is_device_ptr(genes), pout = vdi::is_device_ptr(poses);
+    if (!gin) {
+        VD_CK(cudaMallocAsync((void **)&dg, P * ngenes * sizeof(double), st));
+        VD_CK(cudaMemcpyAsync((void *)dg, genes, P * ngenes * sizeof(double), cudaMemcpyHostToDevice, st));
+    }
+    if (!pout) VD_CK(cudaMallocAsync((void **)&dp, P * 3 * L.n_atoms * sizeof(float), st));
+    VD_CK(vd::launch_pose(L, dg, P, ngenes, dp, st));
+    if (!pout) {
+        VD_CK(cudaMemcpyAsync(poses, dp, P * 3 * L.n_atoms * sizeof(float), cudaMemcpyDeviceToHost, st));
+        VD_CK(cudaFreeAsync(dp, st));
+    }
+    if (!gin) VD_CK(cudaFreeAsync((void *)dg, st));
+    if (!pout) VD_CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,380 @@
+/*
+ * vd_ga.cu -- the whole GA of vd/ga.py:180-235 on the device, for a batch of
+ * ligands (vd/screening.py:165-244 semantics, ligand i keyed (seed, base+i)).
+ *
+ * Persistent CTAs pull ligands from an atomic work counter (host passes a
+ * largest-first order), so ligands of very different sizes balance across
+ * the 148 SMs.  One CTA runs one ligand's GA for all generations:
+ *   score   thread-per-individual fused pose+inter+intra (vd_device.cuh)
+ *   select  block arg-min for the generation best / elites (first index on ties)
+ *   breed   thread-per-child tournament, two-point crossover, Gaussian
+ *           mutation, quaternion renormalisation (vd/ga.py:120-177)
+ * Genes live in a CTA-private double buffer in global memory (L2-resident);
+ * only the pose tile, fitness and the per-generation scratch sit in shared
+ * memory.  All randomness comes from vd_rng.h's counter-addressed
+ * Philox4x64-10 with IEEE-exact transforms, identical to the CPU oracle's.
+ */
+#include <algorithm>
+#include <vector>
+
+#include "vd_internal.h"
+#include "vd_rng.h"
+
+namespace vd {
+
+struct GaDev {
+    int pop, generations, tournament, elitism;
+    double cx_rate, mut_rate, sigma_t, sigma_r, sigma_tor;
+    double lo[3], hi[3];
+};
+
+struct GaOut {
+    float *best_total;
+    double *best_inter, *best_intra, *best_genes;
+    int gstride;
+    float *trace;
+    int64_t *n_evals;
+};
+
+/* block-wide (value, index) arg-min, first index on ties; `skip` flags excluded */
+__device__ int block_argmin(const float *v, const unsigned char *skip, int n, int *s_idx,
+                            float *s_val)
+{
+    float bv = INFINITY;
+    int bi = -1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        if (skip && skip[i]) continue;
+        const float x = v[i];
+        if (bi < 0 || x < bv) { bv = x; bi = i; }  /* strided ascending: first min kept */
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_down_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && (bi < 0 || ov < bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { s_val[warp] = bv; s_idx[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        float v0 = s_val[0];
+        int i0 = s_idx[0];
+        for (int w = 1; w < nw; ++w) {
+            const int oi = s_idx[w];
+            const float ov = s_val[w];
+            if (oi >= 0 && (i0 < 0 || ov < v0 || (ov == v0 && oi < i0))) { v0 = ov; i0 = oi; }
+        }
+        s_idx[32] = i0;
+    }
+    __syncthreads();
+    const int r = s_idx[32];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ double dquat_norm(const double *q)
+{
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q[0], q[0]), __dmul_rn(q[1], q[1])),
+                                          __dmul_rn(q[2], q[2])), __dmul_rn(q[3], q[3])));
+}
+
+__device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0, uint64_t k1, double *g)
+{
+    const double PI = 3.141592653589793;
+    for (int a = 0; a < 3; ++a) {
+        const double u = vd_u01(vd_word(a, i, 0, VD_PH_INIT_U, k0, k1));
+        g[a] = __dadd_rn(P.lo[a], __dmul_rn(__dsub_rn(P.hi[a], P.lo[a]), u));
+    }
+    double q[4];
+    for (int c = 0; c < 4; ++c) q[c] = vd_normal(c, i, 0, VD_PH_INIT_N, k0, k1);
+    double n = dquat_norm(q);
+    if (n < 1e-12) { q[0] = 1.0; q[1] = q[2] = q[3] = 0.0; n = 1.0; }
+    for (int c = 0; c < 4; ++c) g[3 + c] = __ddiv_rn(q[c], n);
+    for (int t = 0; t < T; ++t) {
+        const double u = vd_u01(vd_word(4 + t, i, 0, VD_PH_INIT_U, k0, k1));
+        g[7 + t] = __dadd_rn(-PI, __dmul_rn(2.0 * PI, u));
+    }
+}
+
+__device__ void breed_child(const GaDev &P, int G, const double *cur, const float *fit, int gen,
+                            int c, uint64_t k0, uint64_t k1, double *child)
+{
+    const int k = P.tournament;
+    int win[2];
+    for (int r = 0; r < 2; ++r) {
+        int best = -1;
+        for (int j = 0; j < k; ++j) {
+            const int idx = (int)vd_below(vd_word(r * k + j, c, gen, VD_PH_BREED_U, k0, k1),
+                                          (uint64_t)P.pop);
+            if (best < 0 || fit[idx] < fit[best]) best = idx;
+        }
+        win[r] = best;
+    }
+    const double *p1 = cur + (size_t)win[0] * G, *p2 = cur + (size_t)win[1] * G;
+    const bool do_cx = vd_u01(vd_word(2 * k, c, gen, VD_PH_BREED_U, k0, k1)) < P.cx_rate;
+    const int a = (int)vd_below(vd_word(2 * k + 1, c, gen, VD_PH_BREED_U, k0, k1), (uint64_t)G + 1);
+    const int b = (int)vd_below(vd_word(2 * k + 2, c, gen, VD_PH_BREED_U, k0, k1), (uint64_t)G + 1);
+    const int c_lo = min(a, b), c_hi = max(a, b);
+    bool mut_rot = false;
+    for (int g = 0; g < G; ++g) {
+        const double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
+        const bool mut = vd_u01(vd_word(2 * k + 3 + g, c, gen, VD_PH_BREED_U, k0, k1)) < P.mut_rate;
+        double noise = 0.0;
+        if (mut) {
+            const double sig = g < 3 ? P.sigma_t : (g < 7 ? P.sigma_r : P.sigma_tor);
+            noise = __dmul_rn(vd_normal(g, c, gen, VD_PH_BREED_N, k0, k1), sig);
+            mut_rot |= (g >= 3 && g < 7);
+        }
+        child[g] = __dadd_rn(v, noise);
+    }
+    double n = dquat_norm(child + 3);
+    const bool bad = n < 1e-9;
+    if (bad) {
+        for (int q = 3; q < 7; ++q) child[q] = p1[q];
+        n = dquat_norm(child + 3);
+    }
+    if (mut_rot || bad)
+        for (int q = 3; q < 7; ++q) child[q] = __ddiv_rn(child[q], n);
+}
+
+struct GaLayout {
+    int nmax;                 /* atoms of the largest ligand: pose tile is [3][nmax][B] f32 */
+    unsigned off_fit, off_e, off_a, off_taken, bytes;
+};
+
+template <bool EXACT, int B>
+__global__ void __launch_bounds__(B) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+                                               const int *__restrict__ order, int count, GaDev P,
+                                               uint64_t seed, int64_t base, int *work,
+                                               double *gene_buf, int gmax, GaLayout lay, GaOut out)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *S = reinterpret_cast<float *>(smem) + threadIdx.x;
+    float *fit = reinterpret_cast<float *>(smem + lay.off_fit);
+    double *e64 = reinterpret_cast<double *>(smem + lay.off_e);
+    double *a64 = reinterpret_cast<double *>(smem + lay.off_a);
+    unsigned char *taken = smem + lay.off_taken;
+    __shared__ int s_lig, s_best;
+    __shared__ int s_idx[33];
+    __shared__ float s_val[32];
+    const int pop = P.pop;
+    double *buf0 = gene_buf + (size_t)blockIdx.x * 2 * pop * gmax;
+    double *buf1 = buf0 + (size_t)pop * gmax;
+    for (;;) {
+        if (threadIdx.x == 0) s_lig = atomicAdd(work, 1);
+        __syncthreads();
+        const int slot = s_lig;
+        __syncthreads();
+        if (slot >= count) break;
+        const int l = order ? order[slot] : slot;
+        const LigView L = ligs[l];
+        const int T = L.n_torsions, G = 7 + T;
+        const uint64_t k0 = seed, k1 = (uint64_t)(base + l);
+        double *cur = buf0, *nxt = buf1;
+        for (int i = threadIdx.x; i < pop; i += B) init_individual(P, T, i, k0, k1, cur + (size_t)i * G);
+        float best_total = INFINITY;
+        bool have = false;
+        __syncthreads();
+        for (int gen = 0; gen <= P.generations; ++gen) {
+            for (int i = threadIdx.x; i < pop; i += B) {
+                build_pose<B>(L, cur + (size_t)i * G, S);
+                const double e = inter_energy<EXACT, B>(L, Gv, S);
+                const double a = L.n_pairs ? intra_energy<EXACT, B>(L, S) : 0.0;
+                e64[i] = e;
+                a64[i] = a;
+                fit[i] = total32(e, a, L.tors32);
+            }
+            __syncthreads();
+            const int idx = block_argmin(fit, nullptr, pop, s_idx, s_val);
+            const float fb = fit[idx];
+            const bool better = !have || fb < best_total;  /* strict '<' (vd/ga.py:217) */
+            if (better) {
+                for (int g = threadIdx.x; g < G; g += B) out.best_genes[(size_t)l * out.gstride + g] = cur[(size_t)idx * G + g];
+                if (threadIdx.x == 0) {
+                    out.best_total[l] = fb;
+                    out.best_inter[l] = e64[idx];
+                    out.best_intra[l] = a64[idx];
+                }
+                best_total = fb;
+                have = true;
+            }
+            if (out.trace && threadIdx.x == 0) out.trace[(size_t)l * (P.generations + 1) + gen] = fb;
+            if (gen == P.generations) break;
+            /* elites: first `elitism` of a stable ascending sort (vd/ga.py:136-137) */
+            for (int i = threadIdx.x; i < pop; i += B) taken[i] = 0;
+            __syncthreads();
+            for (int e = 0; e < P.elitism; ++e) {
+                const int ei = e == 0 ? idx : block_argmin(fit, taken, pop, s_idx, s_val);
+                if (threadIdx.x == 0) { taken[ei] = 1; s_best = ei; }
+                __syncthreads();
+                for (int g = threadIdx.x; g < G; g += B) nxt[(size_t)e * G + g] = cur[(size_t)s_best * G + g];
+                __syncthreads();
+            }
+            for (int c = threadIdx.x; c < pop - P.elitism; c += B)
+                breed_child(P, G, cur, fit, gen, c, k0, k1, nxt + (size_t)(P.elitism + c) * G);
+            __syncthreads();
+            double *t = cur; cur = nxt; nxt = t;
+        }
+        if (threadIdx.x == 0) out.n_evals[l] = (int64_t)pop * (P.generations + 1);
+        __syncthreads();
+    }
+}
+
+template <bool EXACT, int B>
+static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
+                               int count, const GaDev &P, uint64_t seed, int64_t base,
+                               double *gene_buf_dummy, int gmax, const GaLayout &lay,
+                               const GaOut &out, cudaStream_t st, int *d_work, double **gene_buf,
+                               int *n_ctas)
+{
+    (void)gene_buf_dummy;
+    auto k = ga_kernel<EXACT, B>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, B, lay.bytes);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ctas = std::max(1, std::min(count, std::max(1, per_sm) * sms));
+    e = cudaMallocAsync((void **)gene_buf, sizeof(double) * (size_t)ctas * 2 * P.pop * gmax, st);
+    if (e != cudaSuccess) return e;
+    k<<<ctas, B, lay.bytes, st>>>(Gv, d_ligs, d_order, count, P, seed, base, d_work, *gene_buf, gmax, lay, out);
+    ++vdi::g_launches;
+    *n_ctas = ctas;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ga(int mode, int B, const GridView &Gv, const LigView *d_ligs,
+                      const int *d_order, int count, const GaDev &P, uint64_t seed, int64_t base,
+                      int gmax, const GaLayout &lay, const GaOut &out, cudaStream_t st,
+                      int *d_work, double **gene_buf, int *n_ctas)
+{
+#define VD_GA_CASE(EX, BB) \
+    return launch_ga_t<EX, BB>(Gv, d_ligs, d_order, count, P, seed, base, nullptr, gmax, lay, out, st, d_work, gene_buf, n_ctas)
+    if (mode == VD_MODE_EXACT) {
+        if (B == 128) VD_GA_CASE(true, 128);
+        if (B == 64) VD_GA_CASE(true, 64);
+        VD_GA_CASE(true, 32);
+    }
+    if (B == 128) VD_GA_CASE(false, 128);
+    if (B == 64) VD_GA_CASE(false, 64);
+    VD_GA_CASE(false, 32);
+#undef VD_GA_CASE
+}
+
+}  // namespace vd
+
+using vdi::set_error;
+
+extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, int count,
+                             const vd_ga_params *p, uint64_t seed, int64_t lig_index_base,
+                             int mode, float *best_total, double *best_inter, double *best_intra,
+                             double *best_genes, int gstride, float *trace, int64_t *n_evals,
+                             void *stream)
+{
+    if (!g || !s || !p || first < 0 || count < 0 || first + count > s->n_ligands) {
+        set_error("vd_dock_batch: bad handle or ligand range");
+        return -1;
+    }
+    if (count == 0) return 0;
+    if (p->pop < 2 || p->elitism < 0 || p->elitism >= p->pop || p->tournament < 1 ||
+        p->generations < 0) {
+        set_error("vd_dock_batch: invalid GA parameters");
+        return -1;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    /* ligand views + largest-first order */
+    std::vector<vd::LigView> views(count);
+    std::vector<int> order(count);
+    int nmax = 1, tmax = 0;
+    for (int l = 0; l < count; ++l) {
+        views[l] = s->view(first + l);
+        nmax = std::max(nmax, views[l].n_atoms);
+        tmax = std::max(tmax, views[l].n_torsions);
+        order[l] = l;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        const int64_t ca = (int64_t)views[a].n_pairs + 4 * views[a].n_atoms;
+        const int64_t cb = (int64_t)views[b].n_pairs + 4 * views[b].n_atoms;
+        return ca > cb;
+    });
+    const int gmax = 7 + tmax;
+    if (gstride < gmax) {
+        set_error("vd_dock_batch: gstride smaller than 7 + max torsions");
+        return -1;
+    }
+    int B;
+    if (vdi::pick_block(nmax, &B)) return -1;
+    vd::GaLayout lay;
+    lay.nmax = nmax;
+    unsigned off = (unsigned)(sizeof(float) * 3 * (size_t)nmax * B);
+    off = (off + 15) & ~15u;
+    lay.off_fit = off;
+    off += sizeof(float) * p->pop;
+    off = (off + 15) & ~15u;
+    lay.off_e = off;
+    off += sizeof(double) * p->pop;
+    lay.off_a = off;
+    off += sizeof(double) * p->pop;
+    lay.off_taken = off;
+    off += p->pop;
+    lay.bytes = (off + 15) & ~15u;
+    if (lay.bytes > 227 * 1024) {
+        set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
+        return -1;
+    }
+    vd::GaDev P;
+    P.pop = p->pop; P.generations = p->generations; P.tournament = p->tournament;
+    P.elitism = p->elitism;
+    P.cx_rate = p->cx_rate; P.mut_rate = p->mut_rate;
+    P.sigma_t = p->sigma_t; P.sigma_r = p->sigma_r; P.sigma_tor = p->sigma_tor;
+    for (int k = 0; k < 3; ++k) { P.lo[k] = p->lo[k]; P.hi[k] = p->hi[k]; }
+
+    const bool dev_out = vdi::is_device_ptr(best_total);
+    vd::LigView *d_views = nullptr;
+    int *d_order = nullptr, *d_work = nullptr;
+    double *gene_buf = nullptr;
+    float *d_bt = best_total, *d_tr = trace;
+    double *d_be = best_inter, *d_ba = best_intra, *d_bg = best_genes;
+    int64_t *d_ne = n_evals;
+    const size_t G1 = (size_t)p->generations + 1;
+    VD_CK(cudaMallocAsync((void **)&d_views, sizeof(vd::LigView) * count, st));
+    VD_CK(cudaMallocAsync((void **)&d_order, sizeof(int) * count, st));
+    VD_CK(cudaMallocAsync((void **)&d_work, sizeof(int), st));
+    VD_CK(cudaMemcpyAsync(d_views, views.data(), sizeof(vd::LigView) * count, cudaMemcpyHostToDevice, st));
+    VD_CK(cudaMemcpyAsync(d_order, order.data(), sizeof(int) * count, cudaMemcpyHostToDevice, st));
+    VD_CK(cudaMemsetAsync(d_work, 0, sizeof(int), st));
+    if (!dev_out) {
+        VD_CK(cudaMallocAsync((void **)&d_bt, sizeof(float) * count, st));
+        VD_CK(cudaMallocAsync((void **)&d_be, sizeof(double) * count, st));
+        VD_CK(cudaMallocAsync((void **)&d_ba, sizeof(double) * count, st));
+        VD_CK(cudaMallocAsync((void **)&d_bg, sizeof(double) * count * gstride, st));
+        VD_CK(cudaMallocAsync((void **)&d_ne, sizeof(int64_t) * count, st));
+        if (trace) VD_CK(cudaMallocAsync((void **)&d_tr, sizeof(float) * count * G1, st));
+    }
+    VD_CK(cudaMemsetAsync(d_bg, 0, sizeof(double) * count * gstride, st));
+    vd::GaOut o;
+    o.best_total = d_bt; o.best_inter = d_be; o.best_intra = d_ba; o.best_genes = d_bg;
+    o.gstride = gstride; o.trace = d_tr; o.n_evals = d_ne;
+    int n_ctas = 0;
+    VD_CK(vd::launch_ga(mode, B, vdi::grid_view(g), d_views, d_order, count, P, seed,
+                        lig_index_base, gmax, lay, o, st, d_work, &gene_buf, &n_ctas));
+    if (!dev_out) {
+        VD_CK(cudaMemcpyAsync(best_total, d_bt, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
+        VD_CK(cudaMemcpyAsync(best_inter, d_be, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+        VD_CK(cudaMemcpyAsync(best_intra, d_ba, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+        VD_CK(cudaMemcpyAsync(best_genes, d_bg, sizeof(double) * count * gstride, cudaMemcpyDeviceToHost, st));
+        VD_CK(cudaMemcpyAsync(n_evals, d_ne, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+        if (trace) VD_CK(cudaMemcpyAsync(trace, d_tr, sizeof(float) * count * G1, cudaMemcpyDeviceToHost, st));
+        cudaFreeAsync(d_bt, st); cudaFreeAsync(d_be, st); cudaFreeAsync(d_ba, st);
+        cudaFreeAsync(d_bg, st); cudaFreeAsync(d_ne, st);
+        if (trace) cudaFreeAsync(d_tr, st);
+    }
+    cudaFreeAsync(gene_buf, st);
+    cudaFreeAsync(d_views, st);
+    cudaFreeAsync(d_order, st);
+    cudaFreeAsync(d_work, st);
+    if (!dev_out) VD_CK(cudaStreamSynchronize(st));
+    return 0;
+}

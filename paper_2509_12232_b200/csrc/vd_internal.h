@@ -1,0 +1,47 @@
+/* vd_internal.h -- handle layouts and helpers shared by the .cu files of libvdb200. */
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "vd_device.cuh"
+#include "vecdock_b200.h"
+
+struct vd_grid {
+    int device;
+    int n_maps, nx, ny, nz;
+    float lo[3], hi[3], spacing;
+    float *d_maps;           /* (n_maps, nx, ny, nz) */
+};
+
+struct vd_ligands {
+    int device;
+    int n_ligands;
+    std::vector<int> atom_start, pair_start, tors_start;  /* host copies of the CSR */
+    std::vector<float> tors32, cut2, penalty;
+    int elec_map, desolv_map;
+    int max_atoms, max_torsions;
+    float4 *d_atom;
+    float2 *d_atom2;
+    uint32_t *d_pij;
+    float4 *d_pcoef;
+    int4 *d_tors;
+    int *d_frag;
+    vd::LigView view(int lig) const;
+};
+
+namespace vdi {
+void set_error(const std::string &msg);
+bool check(cudaError_t e, const char *what);
+bool is_device_ptr(const void *p);
+extern thread_local int64_t g_launches;
+vd::GridView grid_view(const vd_grid *g);
+int pick_block(int n_atoms, int *block);  /* poses per CTA for an atom count */
+}  // namespace vdi
+
+#define VD_CK(call)                                        \
+    do {                                                   \
+        if (!vdi::check((call), #call)) return -1;         \
+    } while (0)

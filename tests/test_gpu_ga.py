@@ -1,0 +1,175 @@
+"""GPU GA: device docking vs the restated CPU GA oracle, plus the reference's GA
+contract (pkg/tests/test_ga.py:135-228, test_acceptance.py:211-248)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    from paper_2509_12232_b200.backend import CudaBackend
+
+    return {"fast": CudaBackend(mode="fast", device=0), "exact": CudaBackend(mode="exact", device=0)}
+
+
+def _oracle_dock(c, cfg, seed, lig_index=0):
+    lo, hi = c["grid"].spec.origin, c["grid"].spec.upper
+    return oracle.dock(oracle.Ligand(c["ctx"]), oracle.ga_params(cfg, lo, hi), seed, lig_index)
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1", "rigid", "refgen"])
+def test_exact_mode_ga_is_stream_exact(cuda, name):
+    """Same Philox stream + reference-exact scoring => identical trajectories."""
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    c = fx.pop_case(name)
+    cfg = GaConfig(population_size=48, generations=12, seed=5)
+    res = dock(c["topo"], c["grid"], cfg, backend=cuda["exact"], context=c["ctx"])
+    g, bt, be, ba, trace, ne = _oracle_dock(c, cfg, 5)
+    assert np.array_equal(res.trace.view(np.uint32), trace.view(np.uint32))
+    assert np.array_equal(res.best_genotype, g)
+    assert res.best_score.total == float(bt)
+    assert res.n_evaluations == ne == 48 * 13
+
+
+@pytest.mark.parametrize("name", ["cfg0", "cfg1"])
+def test_fast_mode_ga_within_tolerance_or_rmsd(cuda, name):
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    c = fx.pop_case(name)
+    cfg = GaConfig(population_size=64, generations=30, seed=11)
+    res = dock(c["topo"], c["grid"], cfg, backend=cuda["fast"], context=c["ctx"])
+    g, bt, *_ = _oracle_dock(c, cfg, 11)
+    if not fx.within_tol([res.best_score.total], [bt]).all():
+        lig = oracle.Ligand(c["ctx"])
+        p_dev = oracle.pose_population(lig, res.best_genotype[None])[0]
+        p_ref = oracle.pose_population(lig, g[None])[0]
+        rmsd = float(np.sqrt(((p_dev - p_ref) ** 2).sum(axis=0).mean()))
+        assert rmsd <= 0.5, (res.best_score.total, bt, rmsd)
+
+
+def test_contract_monotone_trace_count_determinism(cuda):
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    c = fx.pop_case("cfg0")
+    cfg = GaConfig(population_size=16, generations=25, seed=2)
+    r1 = dock(c["topo"], c["grid"], cfg, backend=cuda["fast"], context=c["ctx"])
+    r2 = dock(c["topo"], c["grid"], cfg, backend=cuda["fast"], context=c["ctx"])
+    assert np.all(np.diff(r1.trace) <= 0)
+    assert len(r1.trace) == cfg.generations + 1
+    assert r1.n_evaluations == 16 * 26
+    assert np.array_equal(r1.best_genotype, r2.best_genotype)
+    assert np.array_equal(r1.trace.view(np.uint32), r2.trace.view(np.uint32))
+    r3 = dock(c["topo"], c["grid"], GaConfig(population_size=16, generations=25, seed=3),
+              backend=cuda["fast"], context=c["ctx"])
+    assert not np.array_equal(r1.best_genotype, r3.best_genotype)
+    from paper_2509_12232_b200 import backend
+
+    re = backend.score_pose(c["topo"], r1.best_genotype, c["grid"], backend=cuda["fast"],
+                            context=c["ctx"])
+    assert re.total == pytest.approx(r1.best_score.total, abs=1e-4)
+
+
+def test_constant_landscape_trace(cuda):
+    from paper_2509_12232_b200 import chem, gridmaps, topology
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    custom = chem.parse_parameter_table("C 4.0 0.0 0.0 0.0 0\n")
+    spec = gridmaps.GridSpec.centered((0, 0, 0), (5, 5, 5), 1.0)
+    z = np.zeros(spec.dims, np.float32)
+    gset = gridmaps.GridMapSet(spec, {"C": z, chem.ELEC_LABEL: z, chem.DESOLV_LABEL: z})
+    coords = np.zeros((3, 3), np.float32)
+    coords[0] = [-1.0, 0.0, 1.0]
+    topo = topology.LigandTopology(coords, np.zeros(3, np.int32), np.zeros(3, np.float32),
+                                   np.array([[0, 1], [1, 2]], np.int32),
+                                   (topology.RotatableBond(0, 1, np.array([1, 2], np.int32)),))
+    res = dock(topo, gset, GaConfig(population_size=10, generations=15, seed=1),
+               backend=cuda["fast"], table=custom)
+    assert np.all(res.trace == float(np.float32(chem.TermWeights().tors)))
+
+
+def test_single_atom_converges_to_minimum_node(cuda):
+    """pkg/tests/test_ga.py:195-228: 20/20 seeds park the atom within 2 spacings."""
+    from paper_2509_12232_b200 import chem, gridmaps, topology
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    custom = chem.parse_parameter_table("C 4.0 0.0 0.0 0.0 0\n")
+    spec = gridmaps.GridSpec.centered((0, 0, 0), (9, 9, 9), 0.5)
+    target = (6, 3, 2)
+    ax, ay, az = np.meshgrid(np.arange(9), np.arange(9), np.arange(9), indexing="ij")
+    m = (0.5 * np.sqrt((ax - 6.0) ** 2 + (ay - 3.0) ** 2 + (az - 2.0) ** 2)).astype(np.float32)
+    m[target] = -50.0
+    z = np.zeros(spec.dims, np.float32)
+    gset = gridmaps.GridMapSet(spec, {"C": m, chem.ELEC_LABEL: z, chem.DESOLV_LABEL: z})
+    topo = topology.LigandTopology(np.zeros((3, 1), np.float32), np.zeros(1, np.int32),
+                                   np.zeros(1, np.float32), np.empty((0, 2), np.int32))
+    txyz = np.array([spec.origin[k] + target[k] * spec.spacing for k in range(3)])
+    hits = 0
+    for seed in range(20):
+        cfg = GaConfig(population_size=40, generations=200, seed=seed, elitism_count=1)
+        r = dock(topo, gset, cfg, backend=cuda["fast"], table=custom)
+        hits += np.linalg.norm(r.best_genotype[:3] - txyz) <= 2 * spec.spacing
+    assert hits == 20
+
+
+def test_batch_equals_single_and_is_shard_independent(cuda):
+    """Ligand i keyed (seed, i): one batched launch == per-ligand launches == any split."""
+    from paper_2509_12232_b200 import synth
+    from paper_2509_12232_b200.ga import GaConfig
+    from paper_2509_12232_b200.screening import ScreenConfig, screen_batch
+
+    c = fx.pop_case("cfg1")
+    ligs = [(f"l{i}", synth.config_ligand(2, i)) for i in range(12)]
+    cfg = ScreenConfig(ga=GaConfig(population_size=32, generations=8), backend="cuda",
+                       global_seed=4)
+    whole = screen_batch(ligs, c["grid"], cfg)
+    from paper_2509_12232_b200 import ga as gam
+
+    for i in (0, 5, 11):
+        r = gam.dock(ligs[i][1], c["grid"], cfg.ga, backend="cuda", seed_key=(4, i))
+        assert np.array_equal(r.best_genotype, whole[i].result.best_genotype)
+        assert r.best_score == whole[i].result.best_score
+    # emulate a 3-rank split: each shard docked by its own launch with its global base
+    from dataclasses import replace
+
+    from paper_2509_12232_b200 import backend as bk
+    from paper_2509_12232_b200.context import prepare_context
+    from paper_2509_12232_b200.screening import _shared_device_set, shard_range
+
+    b = bk.get_backend("cuda")
+    ctxs = [prepare_context(t, c["grid"]) for _, t in ligs]
+    grid, lset = _shared_device_set(b, c["grid"], ctxs)
+    ga = replace(cfg.ga, translation_bounds=(c["grid"].spec.origin, c["grid"].spec.upper))
+    gmax = 7 + max(t.n_torsions for _, t in ligs)
+    full = gam._run(grid, lset, 0, len(ligs), ga, 4, 0, b._mode(), gmax, trace=False)
+    for rank in range(3):
+        lo, hi = shard_range(len(ligs), rank, 3)
+        part = gam._run(grid, lset, lo, hi - lo, ga, 4, lo, b._mode(), gmax, trace=False)
+        assert np.array_equal(part[3], full[3][lo:hi])
+        assert np.array_equal(part[0], full[0][lo:hi])
+
+
+def test_exact_batch_matches_oracle_dock_many(cuda):
+    from paper_2509_12232_b200 import synth
+    from paper_2509_12232_b200.context import prepare_context
+    from paper_2509_12232_b200.ga import GaConfig
+    from paper_2509_12232_b200.screening import ScreenConfig, screen_batch
+
+    c = fx.pop_case("cfg1")
+    ligs = [(f"l{i}", synth.config_ligand(2, i)) for i in range(6)]
+    ga = GaConfig(population_size=24, generations=6)
+    got = screen_batch(ligs, c["grid"], ScreenConfig(ga=ga, backend="cuda-exact", global_seed=9))
+    lo, hi = c["grid"].spec.origin, c["grid"].spec.upper
+    ors = [oracle.Ligand(prepare_context(t, c["grid"])) for _, t in ligs]
+    g, bt, be, ba, ne = oracle.dock_many(ors, oracle.ga_params(ga, lo, hi), 9, 0)
+    for i, e in enumerate(got):
+        G = 7 + ligs[i][1].n_torsions
+        assert np.array_equal(e.result.best_genotype, g[i, :G])
+        assert e.result.best_score.total == float(bt[i])

@@ -1,0 +1,239 @@
+"""GPU parity: the CUDA scoring path (through the C-ABI) against the reference
+fixtures and the CPU oracle.  Restates the reference's scoring contract tests
+(pkg/tests/test_scoring.py) for the `cuda` backend.
+
+Tolerances: EXACT mode reproduces the reference's canonical sequences and
+must agree to 1e-6 relative (in practice bit-for-bit); FAST mode must meet
+the north-star rule |d| <= 1e-3 kcal/mol or |d|/|E| <= 1e-4 per pose.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import fixtures as fx
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def cuda():
+    from paper_2509_12232_b200.backend import CudaBackend
+
+    return {"fast": CudaBackend(mode="fast", device=0), "exact": CudaBackend(mode="exact", device=0)}
+
+
+def test_native_library_is_the_one_loaded():
+    from paper_2509_12232_b200 import _abi
+
+    lib = _abi.lib()
+    assert lib._name.endswith("libvdb200.so")
+    assert _abi.launches() >= 0
+
+
+@pytest.mark.parametrize("name", fx.POP_NAMES)
+def test_poses_bitwise_vs_reference(cuda, name):
+    c = fx.pop_case(name)
+    got = cuda["exact"].pose_population(c["genes"][: len(c["poses"])], c["ctx"])
+    assert np.array_equal(got.view(np.uint32), c["poses"].view(np.uint32))
+
+
+@pytest.mark.parametrize("name", fx.POP_NAMES)
+def test_exact_mode_matches_reference(cuda, name):
+    c = fx.pop_case(name)
+    e, a, t = cuda["exact"].score_population_arrays(c["genes"], c["ctx"])
+    for got, want in ((e, c["inter"]), (a, c["intra"]), (t.astype(np.float64), c["total"])):
+        rel = np.abs(got - want) / np.maximum(1.0, np.abs(want))
+        assert rel.max() <= 1e-6, rel.max()
+    # bit-exact on (nearly) every pose: only libm ulp differences may flip a rounding
+    assert np.mean(t.view(np.uint32) == c["total"].view(np.uint32)) >= 0.99
+
+
+@pytest.mark.parametrize("name", fx.POP_NAMES)
+def test_fast_mode_within_north_star_tolerance(cuda, name):
+    c = fx.pop_case(name)
+    e, a, t = cuda["fast"].score_population_arrays(c["genes"], c["ctx"])
+    assert fx.within_tol(t, c["total"]).all()
+    assert fx.within_tol(e, c["inter"]).all()
+    assert fx.within_tol(a, c["intra"]).all()
+
+
+def test_golden_vector(cuda):
+    d, topo, gset, ctx = fx.golden_case()
+    from paper_2509_12232_b200 import backend
+
+    want = d["expected"]
+    for mode in ("fast", "exact"):
+        bd = backend.score_pose(topo, d["genotype"], gset, backend=cuda[mode], context=ctx)
+        got = np.array([bd.inter, bd.intra, bd.torsional, bd.total])
+        assert np.all(np.abs(got - want) / np.maximum(1.0, np.abs(want)) < 1e-4), (mode, got)
+
+
+def test_score_poses_path_matches_fixture(cuda):
+    c = fx.pop_case("cfg0")
+    e, a = cuda["exact"].score_many(c["poses"], c["ctx"])
+    n = len(c["poses"])
+    np.testing.assert_allclose(e, c["inter"][:n], rtol=1e-6)
+    np.testing.assert_allclose(a, c["intra"][:n], rtol=1e-6)
+
+
+def _node_fixture():
+    from paper_2509_12232_b200 import chem, gridmaps, topology
+
+    rng = np.random.default_rng(7)
+    spec = gridmaps.GridSpec(origin=(-2.0, -2.0, -2.0), spacing=0.5, dims=(9, 9, 9))
+    custom = chem.parse_parameter_table("C 4.0 0.15 33.51 0.0 0\n")
+    maps = {"C": rng.uniform(-3, 3, spec.dims).astype(np.float32),
+            chem.ELEC_LABEL: rng.uniform(-3, 3, spec.dims).astype(np.float32),
+            chem.DESOLV_LABEL: rng.uniform(-3, 3, spec.dims).astype(np.float32)}
+    gset = gridmaps.GridMapSet(spec, maps)
+    nodes = [(0, 0, 0), (3, 7, 2), (8, 8, 8), (4, 1, 6)]
+    coords = np.array([[spec.origin[k] + n[k] * spec.spacing for n in nodes] for k in range(3)],
+                      np.float32)
+    topo = topology.LigandTopology(coords, np.zeros(4, np.int32), np.zeros(4, np.float32),
+                                   np.array([[k, k + 1] for k in range(3)], np.int32))
+    return gset, custom, topo, nodes
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_atoms_on_nodes_reproduce_map_values(cuda, mode):
+    """pkg/tests/test_scoring.py:48-71 (node-exact, '==')."""
+    from paper_2509_12232_b200 import backend
+
+    gset, custom, topo, nodes = _node_fixture()
+    got = backend.inter_energy(topo.coords0, topo.type_index, topo.charge, gset,
+                               backend=cuda[mode], table=custom)
+    want = float(np.float32(sum(float(gset.maps["C"][n]) for n in nodes)))
+    assert got == want
+    one = backend.inter_energy(topo.coords0[:, :1], topo.type_index[:1], topo.charge[:1], gset,
+                               backend=cuda[mode], table=custom)
+    assert one == float(gset.maps["C"][nodes[0]])
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_out_of_box_penalty(cuda, mode):
+    """pkg/tests/test_scoring.py:73-86."""
+    from paper_2509_12232_b200 import backend
+
+    gset, custom, _, _ = _node_fixture()
+    coords = np.array([[gset.spec.upper[0] + 2.0], [0.0], [0.0]], np.float32)
+    got = backend.inter_energy(coords, np.zeros(1, np.int32), np.zeros(1, np.float32), gset,
+                               backend=cuda[mode], table=custom)
+    assert got == pytest.approx(1e4 * 3.0, rel=1e-6)
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_intra_empty_and_equilibrium_pair(cuda, mode):
+    """pkg/tests/test_scoring.py:101-120."""
+    from paper_2509_12232_b200 import backend, chem, topology
+
+    empty = topology.NonbondPairList.empty()
+    coords = np.zeros((3, 4), np.float32)
+    coords[0] = [0, 1.5, 3.0, 4.5]
+    assert backend.intra_energy(coords, empty, backend=cuda[mode]) == 0.0
+    custom = chem.parse_parameter_table("C 4.0 0.15 0.0 0.0 0\n")
+    c5 = np.zeros((3, 5), np.float32)
+    c5[0] = [0.0, 1.0, 2.0, 3.0, 4.0]
+    topo = topology.LigandTopology(c5, np.zeros(5, np.int32), np.zeros(5, np.float32),
+                                   np.array([[k, k + 1] for k in range(4)], np.int32))
+    pl = topology.build_nonbond_pairlist(topo, custom)
+    assert pl.pairs() == [(0, 4)]
+    w = chem.TermWeights()
+    got = backend.intra_energy(topo.coords0, pl, weights=w, backend=cuda[mode])
+    assert got == pytest.approx(w.vdw * -0.15, rel=1e-5)
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_constant_landscape_only_torsional(cuda, mode):
+    """pkg/tests/test_scoring.py:176-200."""
+    from paper_2509_12232_b200 import backend, chem, gridmaps, topology
+
+    custom = chem.parse_parameter_table("C 4.0 0.0 0.0 0.0 0\n")
+    spec = gridmaps.GridSpec.centered((0, 0, 0), (9, 9, 9), 1.0)
+    z = np.zeros(spec.dims, np.float32)
+    gset = gridmaps.GridMapSet(spec, {"C": z, chem.ELEC_LABEL: z, chem.DESOLV_LABEL: z})
+    coords = np.zeros((3, 3), np.float32)
+    coords[0] = [0.0, 1.0, 2.0]
+    topo = topology.LigandTopology(coords, np.zeros(3, np.int32), np.zeros(3, np.float32),
+                                   np.array([[0, 1], [1, 2]], np.int32),
+                                   (topology.RotatableBond(0, 1, np.array([1, 2], np.int32)),))
+    w = chem.TermWeights()
+    bd = backend.score_pose(topo, np.array([0, 0, 0, 1.0, 0, 0, 0, 0.4]), gset, weights=w,
+                            backend=cuda[mode], table=custom)
+    assert bd.inter == 0.0 and bd.intra == 0.0
+    assert bd.total == float(np.float32(w.tors * 1))
+
+
+def test_intra_invariant_under_rigid_change(cuda):
+    """pkg/tests/test_scoring.py:202-211 / test_acceptance.py geometry invariants."""
+    c = fx.pop_case("cfg1")
+    rng = np.random.default_rng(23)
+    T = c["ctx"].n_torsions
+    tors = rng.uniform(-math.pi, math.pi, T)
+    rows = [np.concatenate([rng.uniform(-2, 2, 3), rng.normal(size=4), tors]) for _ in range(16)]
+    _, a, _ = cuda["fast"].score_population_arrays(np.array(rows), c["ctx"])
+    assert np.max(np.abs(a - a[0]) / max(1.0, abs(a[0]))) < 1e-4
+
+
+def test_large_batch_vs_oracle_and_pipeline(cuda):
+    """300k cfg1-like random poses (crosses the 2^17-pose host pipeline chunk) vs oracle."""
+    from paper_2509_12232_b200 import synth
+
+    c = fx.pop_case("cfg1")
+    spec = c["grid"].spec
+    genes = synth.random_genes(0, 300_000, c["ctx"].n_torsions, spec.origin, spec.upper)
+    e, a, t = cuda["fast"].score_population_arrays(genes, c["ctx"])
+    sub = slice(0, 300_000, 7)
+    we, wa, wt = oracle.dock_population(oracle.Ligand(c["ctx"]), genes[sub], n_threads=0)
+    assert fx.within_tol(t[sub], wt).all()
+    assert fx.within_tol(e[sub], we).all() and fx.within_tol(a[sub], wa).all()
+
+
+def test_device_pointers_match_host_pointers(cuda):
+    import torch
+
+    c = fx.pop_case("cfg0")
+    g = torch.from_numpy(c["genes"]).cuda()
+    P = g.shape[0]
+    out = (torch.empty(P, dtype=torch.float64, device="cuda"),
+           torch.empty(P, dtype=torch.float64, device="cuda"),
+           torch.empty(P, dtype=torch.float32, device="cuda"))
+    cuda["fast"].score_population_arrays(g, c["ctx"], out=out)
+    torch.cuda.synchronize()
+    e, a, t = cuda["fast"].score_population_arrays(c["genes"], c["ctx"])
+    assert np.array_equal(out[2].cpu().numpy(), t) and np.array_equal(out[0].cpu().numpy(), e)
+
+
+def test_reference_context_accepted(cuda):
+    """A ScoringContext carrying its own map stack (the reference's layout) scores identically."""
+    from paper_2509_12232_b200.context import ScoringContext
+    import dataclasses
+
+    c = fx.pop_case("refgen")
+    ctx = c["ctx"]
+    ref_like = dataclasses.replace(ctx, grid_set=None, explicit_stack=ctx.map_stack)
+    e1, a1, t1 = cuda["exact"].score_population_arrays(c["genes"], ctx)
+    e2, a2, t2 = cuda["exact"].score_population_arrays(c["genes"], ref_like)
+    assert np.array_equal(t1, t2) and np.array_equal(e1, e2) and np.array_equal(a1, a2)
+    assert isinstance(ref_like, ScoringContext)
+
+
+@pytest.mark.parametrize("case", ["a", "b"])
+def test_grid_builder_vs_reference(case):
+    from paper_2509_12232_b200 import chem, gridmaps
+
+    d = fx.load("grids_small")
+    p = f"{case}__"
+    prot = fx.protein_from(d, p)
+    ref = fx.grid_from(d, p)
+    probes = [l for l in ref.maps if not l.startswith("@")]
+    got = gridmaps.build_grid_maps(prot, ref.spec, probes, chem.TermWeights(), fx.TABLE)
+    for label in ref.maps:
+        w = ref.maps[label].astype(np.float64)
+        g = got.maps[label].astype(np.float64)
+        rel = np.abs(g - w) / np.maximum(np.abs(w), 1e-4)
+        assert rel.max() < 1e-4, (label, rel.max())
