@@ -30,6 +30,8 @@ from pathlib import Path
 
 import numpy as np
 
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")  # oracle threads must not spin beside the GPU legs
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -203,15 +205,6 @@ def run_ours(args):
     value = world * N_POSES * args.steps / t_max
     ms_per_step = 1e3 * t_max / args.steps
 
-    # sanity: device results agree with the oracle on a sample (not timed)
-    from oracle import oracle
-
-    sub = slice(0, N_POSES, 997)
-    _, _, wt = oracle.dock_population(oracle.Ligand(ctx), genes_h[sub], n_threads=0)
-    got_t = out_d[2].cpu().numpy()[sub]
-    d = np.abs(got_t.astype(np.float64) - wt)
-    parity_ok = bool(np.all((d <= 1e-3) | (d <= 1e-4 * np.abs(wt))))
-
     # e2e: public API, pinned host genes in, host results out, copies inside the region
     pin_g = torch.from_numpy(genes_h).pin_memory()
     pin_out = (torch.empty(N_POSES, dtype=torch.float64).pin_memory(),
@@ -235,6 +228,15 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         te = float(tt.item())
     e2e_value = world * N_POSES * e2e_steps / te
+
+    # sanity: device results agree with the oracle on a sample (not timed)
+    from oracle import oracle
+
+    sub = slice(0, N_POSES, 997)
+    _, _, wt = oracle.dock_population(oracle.Ligand(ctx), genes_h[sub], n_threads=0)
+    got_t = out_d[2].cpu().numpy()[sub]
+    d = np.abs(got_t.astype(np.float64) - wt)
+    parity_ok = bool(np.all((d <= 1e-3) | (d <= 1e-4 * np.abs(wt))))
 
     fpp = flops_per_pose(ctx)
     achieved = fpp * N_POSES / (t_loc / args.steps) / 1e12

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -50,9 +51,64 @@ bool is_device_ptr(const void *p)
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-vd::GridView grid_view(const vd_grid *g)
+__global__ void pack_zpairs(const float *__restrict__ maps, int64_t n, int nz, float2 *zp)
+{
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const bool last = (k % nz) == nz - 1;
+        zp[k] = make_float2(maps[k], last ? 0.0f : maps[k + 1]);
+    }
+}
+
+__global__ void pack_ed(const float *__restrict__ e, const float *__restrict__ d, int64_t n,
+                        int nz, float4 *ed)
+{
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const bool last = (k % nz) == nz - 1;
+        ed[k] = make_float4(e[k], last ? 0.0f : e[k + 1], d[k], last ? 0.0f : d[k + 1]);
+    }
+}
+
+/* Build the packed gather copy when it stays comfortably L2-resident (126 MB L2). */
+bool make_packed(vd_grid *g)
+{
+    const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
+    const int64_t bytes = nodes * (8 * (int64_t)g->n_maps + 16);
+    if (getenv("VD_NO_PACK") || bytes > (int64_t)96 << 20) return true;
+    if (!check(cudaMalloc(&g->d_zp, sizeof(float2) * nodes * g->n_maps), "alloc zp")) return false;
+    pack_zpairs<<<1184, 256>>>(g->d_maps, nodes * g->n_maps, g->nz, g->d_zp);
+    return check(cudaGetLastError(), "pack zp") && check(cudaDeviceSynchronize(), "pack zp sync");
+}
+
+static const float4 *ed_for(const vd_grid *gc, int e, int d)
+{
+    vd_grid *g = const_cast<vd_grid *>(gc);
+    if (!g->d_zp || e < 0 || d < 0 || e >= g->n_maps || d >= g->n_maps) return nullptr;
+    std::lock_guard<std::mutex> lk(g->ed_lock);
+    auto it = g->d_ed.find({e, d});
+    if (it != g->d_ed.end()) return it->second;
+    const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
+    float4 *p = nullptr;
+    if (cudaMalloc(&p, sizeof(float4) * nodes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    pack_ed<<<1184, 256>>>(g->d_maps + nodes * e, g->d_maps + nodes * d, nodes, g->nz, p);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(p);
+        return nullptr;
+    }
+    g->d_ed[{e, d}] = p;
+    return p;
+}
+
+vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)
 {
     vd::GridView v;
+    v.ed = ed_for(g, elec_map, desolv_map);
+    v.zp = v.ed ? g->d_zp : nullptr;
     v.maps = g->d_maps;
     v.nx = g->nx;
     v.ny = g->ny;
@@ -62,20 +118,6 @@ vd::GridView grid_view(const vd_grid *g)
     v.hi0 = g->hi[0]; v.hi1 = g->hi[1]; v.hi2 = g->hi[2];
     v.spacing = g->spacing;
     return v;
-}
-
-/* Poses per CTA: the [3][N][B] f32 coordinate tile must fit in shared memory. */
-int pick_block(int n_atoms, int *block)
-{
-    const size_t limit = 200 * 1024;
-    for (int b : {128, 64, 32})
-        if ((size_t)12 * n_atoms * b <= limit) {
-            *block = b;
-            return 0;
-        }
-    set_error("ligand too large for the shared-memory pose tile (n_atoms = " +
-              std::to_string(n_atoms) + ")");
-    return -1;
 }
 
 struct Pipe {
@@ -107,10 +149,15 @@ vd::LigView vd_ligands::view(int l) const
     v.n_atoms = atom_start[l + 1] - a0;
     v.n_pairs = pair_start[l + 1] - p0;
     v.n_torsions = tors_start[l + 1] - t0;
+    v.n_frag = n_frag[l];
     v.atom = d_atom + a0;
     v.atom2 = d_atom2 + a0;
     v.pij = d_pij + p0;
     v.pcoef = d_pcoef + p0;
+    v.fcoef = d_fcoef + p0;
+    v.fj = d_fj + p0;
+    v.frow = d_frow + frow_start[l];
+    v.ftile = d_ftile + ftile_start[l];
     v.tors = d_tors + t0;
     v.frag = d_frag;
     v.tors32 = tors32[l];
@@ -172,9 +219,9 @@ int vd_grid_create(const float *maps, int n_maps, int nx, int ny, int nz, const 
         return -1;
     }
     if (maps &&
-        !vdi::check(cudaMemcpy(g->d_maps, maps, n * sizeof(float), cudaMemcpyDefault), "upload maps")) {
-        cudaFree(g->d_maps);
-        delete g;
+        (!vdi::check(cudaMemcpy(g->d_maps, maps, n * sizeof(float), cudaMemcpyDefault), "upload maps") ||
+         !vdi::make_packed(g))) {
+        vd_grid_destroy(g);
         return -1;
     }
     *out = g;
@@ -194,6 +241,8 @@ int vd_grid_destroy(vd_grid *g)
 {
     if (!g) return 0;
     cudaFree(g->d_maps);
+    cudaFree(g->d_zp);
+    for (auto &kv : g->d_ed) cudaFree(kv.second);
     delete g;
     return 0;
 }
@@ -235,6 +284,7 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
         }
         s->max_atoms = std::max(s->max_atoms, n);
         s->max_torsions = std::max(s->max_torsions, T);
+        s->n_frag.push_back(T ? a->frag_hi[t0 + T - 1] - a->frag_lo[t0] : 0);
         s->tors32.push_back(a->torsional32 ? a->torsional32[l] : 0.f);
         s->cut2.push_back(a->intra_cutoff2 ? a->intra_cutoff2[l] : INFINITY);
         s->penalty.push_back(a->penalty_scale ? a->penalty_scale[l] : 1.0e4f);
@@ -275,6 +325,35 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
             }
         }
     }
+    /* fast order: stable partition by the 12-10 flag, rows = runs of equal i,
+       rows cut at kTile boundaries of the ligand-local fast index */
+    std::vector<float4> fcoef(std::max(NP, 1));
+    std::vector<int> fj(std::max(NP, 1));
+    std::vector<int4> frow;
+    std::vector<int> ftile;
+    for (int l = 0; l < L; ++l) {
+        const int p0 = a->pair_start[l], p1 = a->pair_start[l + 1];
+        s->frow_start.push_back((int)frow.size());
+        s->ftile_start.push_back((int)ftile.size());
+        int w = p0;
+        for (int g = 0; g < 2; ++g)
+            for (int k = p0; k < p1; ++k)
+                if ((a->pair_hb[k] ? 1 : 0) == g) {
+                    fcoef[w] = pcoef[k];
+                    fj[w] = a->pair_j[k];
+                    const int i = a->pair_i[k], kl = w - p0;
+                    const bool new_tile = (kl % vd::kTile) == 0;
+                    if (new_tile) ftile.push_back((int)frow.size() - s->frow_start[l]);
+                    if (new_tile || frow.empty() || (int)frow.size() == s->frow_start[l] ||
+                        frow.back().x != i || frow.back().w != g)
+                        frow.push_back(make_int4(i, kl, kl + 1, g));
+                    else
+                        frow.back().z = kl + 1;
+                    ++w;
+                }
+        ftile.push_back((int)frow.size() - s->frow_start[l]);
+    }
+    if (frow.empty()) frow.push_back(make_int4(0, 0, 0, 0));
     bool ok = vdi::check(cudaMalloc(&s->d_atom, atom.size() * sizeof(float4)), "alloc atoms") &&
               vdi::check(cudaMalloc(&s->d_atom2, atom2.size() * sizeof(float2)), "alloc atoms2") &&
               vdi::check(cudaMalloc(&s->d_pij, pij.size() * sizeof(uint32_t)), "alloc pairs") &&
@@ -286,7 +365,15 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
               vdi::check(cudaMemcpy(s->d_pij, pij.data(), pij.size() * sizeof(uint32_t), cudaMemcpyHostToDevice), "up pairs") &&
               vdi::check(cudaMemcpy(s->d_pcoef, pcoef.data(), pcoef.size() * sizeof(float4), cudaMemcpyHostToDevice), "up coef") &&
               vdi::check(cudaMemcpy(s->d_tors, tors.data(), tors.size() * sizeof(int4), cudaMemcpyHostToDevice), "up tors") &&
-              vdi::check(cudaMemcpy(s->d_frag, frag.data(), frag.size() * sizeof(int), cudaMemcpyHostToDevice), "up frag");
+              vdi::check(cudaMemcpy(s->d_frag, frag.data(), frag.size() * sizeof(int), cudaMemcpyHostToDevice), "up frag") &&
+              vdi::check(cudaMalloc(&s->d_fcoef, fcoef.size() * sizeof(float4)), "alloc fcoef") &&
+              vdi::check(cudaMalloc(&s->d_fj, fj.size() * sizeof(int)), "alloc fj") &&
+              vdi::check(cudaMalloc(&s->d_frow, frow.size() * sizeof(int4)), "alloc frow") &&
+              vdi::check(cudaMalloc(&s->d_ftile, ftile.size() * sizeof(int)), "alloc ftile") &&
+              vdi::check(cudaMemcpy(s->d_fcoef, fcoef.data(), fcoef.size() * sizeof(float4), cudaMemcpyHostToDevice), "up fcoef") &&
+              vdi::check(cudaMemcpy(s->d_fj, fj.data(), fj.size() * sizeof(int), cudaMemcpyHostToDevice), "up fj") &&
+              vdi::check(cudaMemcpy(s->d_frow, frow.data(), frow.size() * sizeof(int4), cudaMemcpyHostToDevice), "up frow") &&
+              vdi::check(cudaMemcpy(s->d_ftile, ftile.data(), ftile.size() * sizeof(int), cudaMemcpyHostToDevice), "up ftile");
     if (!ok) {
         vd_ligands_destroy(s);
         return -1;
@@ -310,6 +397,10 @@ int vd_ligands_destroy(vd_ligands *s)
     cudaFree(s->d_pcoef);
     cudaFree(s->d_tors);
     cudaFree(s->d_frag);
+    cudaFree(s->d_fcoef);
+    cudaFree(s->d_fj);
+    cudaFree(s->d_frow);
+    cudaFree(s->d_ftile);
     delete s;
     return 0;
 }
@@ -329,7 +420,7 @@ static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const vo
         return -1;
     }
     const vd::LigView L = s->view(lig);
-    const vd::GridView G = vdi::grid_view(g);
+    const vd::GridView G = vdi::grid_view(g, s->elec_map, s->desolv_map);
     const int ngenes = 7 + L.n_torsions;
     const size_t in_row = in_is_genes ? sizeof(double) * ngenes : sizeof(float) * 3 * L.n_atoms;
     const int src = in_is_genes ? 0 : 1;

@@ -1,22 +1,28 @@
 /*
  * vd_device.cuh -- device stages of the docking hot path (sm_100a).
  *
- * Execution model: thread-per-pose.  All poses of a CTA belong to ONE ligand,
- * so every loop below (atoms, torsions, fragment atoms, pairs) is
- * block-uniform: topology and pair parameters are read with broadcast loads
- * and control flow never diverges except at the in-box test.  Each thread
- * owns one column of a shared-memory coordinate tile
- *     S[(3*atom + axis) * B + tid]
- * so coordinate reads/writes are bank-conflict free and need no barriers.
+ * Execution model.  A CTA scores poses of ONE ligand.  Each thread owns a
+ * PAIR of poses (two genotypes) whose coordinates live side by side as float2
+ * in a shared-memory tile  S[(3*atom + axis) * NPP + pp],  so that the f32
+ * pair arithmetic runs as packed f32x2 instructions (FFMA2/FMUL2/FADD2 on
+ * sm_100a) and every broadcast load of topology or pair parameters
+ * is amortised over two poses.  For large ligands TPP > 1 threads share a
+ * pose pair ("sub" lanes split atoms and pairs; barriers order the torsion
+ * chain), which keeps enough warps resident when 12*N bytes per pose limit
+ * how many poses fit in shared memory.  All loops are CTA-uniform: topology
+ * and pair parameters are broadcast reads, pair parameters are staged in
+ * shared-memory tiles of kTile pairs.
  *
  * Stage parity (reference paths under /root/reference/pkg/src/vecdock):
- *   A1 pose   scoring/simd.py:157-222  bit-exact: __f*_rn / __d*_rn intrinsics
- *             (never contracted), fp64 where the reference uses fp64
- *   A2 inter  scoring/simd.py:89-138   box test and cell index bit-exact
- *             (IEEE division); lerps FMA'd in FAST mode
- *   A3 intra  scoring/simd.py:36-86    EXACT: the canonical sequence with fp64
- *             exp and the lane-8 fp64 summation order; FAST: rsqrt/ex2/rcp on
- *             the MUFU pipe, fp32 partial sums flushed to fp64 every 32 pairs
+ *   A1 pose   scoring/simd.py:157-222   bit-exact in both modes: scalar IEEE
+ *             round-to-nearest intrinsics (__f*_rn, __d*_rn),
+ *             never contracted; fp64 where the reference uses fp64
+ *   A2 inter  scoring/simd.py:89-138    bit-exact arithmetic in both modes (IEEE
+ *             division for the cell index, unfused lerps); FAST: branch-free
+ *   A3 intra  scoring/simd.py:36-86     EXACT: canonical sequence, fp64 exp,
+ *             lane-8 fp64 summation order; FAST: MUFU rsqrt/ex2/rcp + an FMA-pipe
+ *             exp2 polynomial, f32x2
+ *             math over a row-ordered pair stream, fp32 partials -> fp64
  */
 #pragma once
 #include <cuda_runtime.h>
@@ -24,24 +30,69 @@
 
 namespace vd {
 
+constexpr int kTile = 256;  /* pairs per shared-memory tile (multiple of 8) */
+
 struct GridView {
     const float *maps;      /* (n_maps, nx, ny, nz) */
     int nx, ny, nz;
     int64_t mstride;        /* nx * ny * nz */
     float lo0, lo1, lo2, hi0, hi1, hi2, spacing;
+    /* packed gather layout (null when the packed copy would not stay L2-resident):
+     *   zp[m][node] = (v[node], v[node + 1])           z-pair of every map, 8 B
+     *   ed[node]    = (e[n], e[n+1], d[n], d[n+1])      elec + desolv z-pairs, 16 B
+     * -> 4 LDG.64 + 4 LDG.128 per atom instead of 24 scalar gathers */
+    const float2 *zp;
+    const float4 *ed;
 };
 
 struct LigView {
-    int n_atoms, n_pairs, n_torsions;
+    int n_atoms, n_pairs, n_torsions, n_frag;
     const float4 *atom;     /* centered x, y, z, charge */
     const float2 *atom2;    /* desolv factor, map index (int bits) */
-    const uint32_t *pij;    /* i | j << 15 | hb << 31 */
-    const float4 *pcoef;    /* a, b, qq, dsl (weight-folded) */
     const int4 *tors;       /* axis_a, axis_b, frag_lo, frag_hi */
     const int *frag;        /* ligand-local atom indices */
+    /* reference order (EXACT): */
+    const uint32_t *pij;    /* i | j << 15 | hb << 31 */
+    const float4 *pcoef;    /* a, b, qq, dsl (weight-folded) */
+    /* fast order (FAST): pairs grouped by hb flag then row i, rows cut at tiles */
+    const float4 *fcoef;
+    const int *fj;
+    const int4 *frow;       /* i, k0, k1, hb  (k = fast-order pair index) */
+    const int *ftile;       /* [n_tiles + 1]: first row of each tile */
     float tors32, cut2, penalty;
     int elec_map, desolv_map;
 };
+
+/* Copy a ligand's topology into shared memory (all CTA threads; caller syncs).
+ * Returns a view whose topology pointers address shared memory. */
+__device__ __forceinline__ LigView stage_topology(const LigView &L, unsigned char *smem,
+                                                  unsigned off_atom, unsigned off_atom2,
+                                                  unsigned off_tors, unsigned off_frag)
+{
+    LigView V = L;
+    float4 *a = reinterpret_cast<float4 *>(smem + off_atom);
+    float2 *a2 = reinterpret_cast<float2 *>(smem + off_atom2);
+    int4 *t = reinterpret_cast<int4 *>(smem + off_tors);
+    int *f = reinterpret_cast<int *>(smem + off_frag);
+    const int nf = L.n_torsions ? __ldg(&L.tors[L.n_torsions - 1]).w - __ldg(&L.tors[0]).z : 0;
+    const int f0 = L.n_torsions ? __ldg(&L.tors[0]).z : 0;
+    for (int i = threadIdx.x; i < L.n_atoms; i += blockDim.x) {
+        a[i] = __ldg(&L.atom[i]);
+        a2[i] = __ldg(&L.atom2[i]);
+    }
+    for (int i = threadIdx.x; i < L.n_torsions; i += blockDim.x) {
+        int4 r = __ldg(&L.tors[i]);
+        r.z -= f0;
+        r.w -= f0;
+        t[i] = r;
+    }
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) f[i] = __ldg(&L.frag[f0 + i]);
+    V.atom = a;
+    V.atom2 = a2;
+    V.tors = t;
+    V.frag = f;
+    return V;
+}
 
 /* energy constants (vd/energy.py:17-34, folded like vd/scoring/__init__.py:42) */
 constexpr double kDielA = -8.5525;
@@ -50,14 +101,40 @@ constexpr double kDielK = 7.7839;
 constexpr double kLamb = 0.003627 * (78.4 - -8.5525);
 constexpr double kDesolvDenom = 2.0 * 3.6 * 3.6;
 constexpr float kMinR2 = 0.01f;
-constexpr float kLog2e = 1.4426950408889634f;
 
-#define VD_S(i, c) S[(3 * (i) + (c)) * B]
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+/* Exact ops for the bit-exact pose stage, applied per component with scalar
+ * IEEE intrinsics.  Packed f32x2 is NOT usable here: ptxas 12.9 fuses packed
+ * multiply + add into FFMA2 (from __fmul2_rn/__fadd2_rn, from explicit
+ * mul.rn/add.rn.f32x2 PTX, even under --fmad=false), which would break parity
+ * with the reference's unfused float32 sequence. */
+__device__ __forceinline__ float2 mul2(float2 a, float2 b)
+{
+    return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b)
+{
+    return make_float2(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y));
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b)
+{
+    return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
+}
+/* Contractible packed ops for the FAST energy stage. */
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+__device__ __forceinline__ float mufu_rsq(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float mufu_ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+__device__ __forceinline__ float mufu_rcp(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+#define VD_S2(i, c) S[(3 * (i) + (c)) * NPP]
 
 /* ---- A1: pose (bit-exact) ------------------------------------------------ */
-template <int B>
-__device__ __forceinline__ void build_pose(const LigView &L, const double *__restrict__ g,
-                                           float *S)
+__device__ __forceinline__ void rigid_of(const double *__restrict__ g, float *m, float *t)
 {
     const double q0 = g[3], q1 = g[4], q2 = g[5], q3 = g[6];
     const double nrm = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q0, q0), __dmul_rn(q1, q1)),
@@ -67,67 +144,97 @@ __device__ __forceinline__ void build_pose(const LigView &L, const double *__res
     const double xx = __dmul_rn(x, x), yy = __dmul_rn(y, y), zz = __dmul_rn(z, z);
     const double xy = __dmul_rn(x, y), xz = __dmul_rn(x, z), yz = __dmul_rn(y, z);
     const double wx = __dmul_rn(w, x), wy = __dmul_rn(w, y), wz = __dmul_rn(w, z);
-    const float m00 = __double2float_rn(__dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(yy, zz))));
-    const float m01 = __double2float_rn(__dmul_rn(2.0, __dsub_rn(xy, wz)));
-    const float m02 = __double2float_rn(__dmul_rn(2.0, __dadd_rn(xz, wy)));
-    const float m10 = __double2float_rn(__dmul_rn(2.0, __dadd_rn(xy, wz)));
-    const float m11 = __double2float_rn(__dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(xx, zz))));
-    const float m12 = __double2float_rn(__dmul_rn(2.0, __dsub_rn(yz, wx)));
-    const float m20 = __double2float_rn(__dmul_rn(2.0, __dsub_rn(xz, wy)));
-    const float m21 = __double2float_rn(__dmul_rn(2.0, __dadd_rn(yz, wx)));
-    const float m22 = __double2float_rn(__dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(xx, yy))));
-    const float tx = __double2float_rn(g[0]), ty = __double2float_rn(g[1]),
-                tz = __double2float_rn(g[2]);
-    for (int i = 0; i < L.n_atoms; ++i) {
-        const float4 c = __ldg(&L.atom[i]);
-        VD_S(i, 0) = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(m00, c.x), __fmul_rn(m01, c.y)),
-                                         __fmul_rn(m02, c.z)), tx);
-        VD_S(i, 1) = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(m10, c.x), __fmul_rn(m11, c.y)),
-                                         __fmul_rn(m12, c.z)), ty);
-        VD_S(i, 2) = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(m20, c.x), __fmul_rn(m21, c.y)),
-                                         __fmul_rn(m22, c.z)), tz);
+    m[0] = __double2float_rn(__dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(yy, zz))));
+    m[1] = __double2float_rn(__dmul_rn(2.0, __dsub_rn(xy, wz)));
+    m[2] = __double2float_rn(__dmul_rn(2.0, __dadd_rn(xz, wy)));
+    m[3] = __double2float_rn(__dmul_rn(2.0, __dadd_rn(xy, wz)));
+    m[4] = __double2float_rn(__dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(xx, zz))));
+    m[5] = __double2float_rn(__dmul_rn(2.0, __dsub_rn(yz, wx)));
+    m[6] = __double2float_rn(__dmul_rn(2.0, __dsub_rn(xz, wy)));
+    m[7] = __double2float_rn(__dmul_rn(2.0, __dadd_rn(yz, wx)));
+    m[8] = __double2float_rn(__dsub_rn(1.0, __dmul_rn(2.0, __dadd_rn(xx, yy))));
+    t[0] = __double2float_rn(g[0]);
+    t[1] = __double2float_rn(g[1]);
+    t[2] = __double2float_rn(g[2]);
+}
+
+__device__ __forceinline__ void torsion_axis(float2 ax, float2 ay, float2 az, float2 &kx,
+                                             float2 &ky, float2 &kz)
+{
+    float k[2][3];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const double x = (double)(p ? ax.y : ax.x), y = (double)(p ? ay.y : ay.x),
+                     z = (double)(p ? az.y : az.x);
+        const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+        k[p][0] = __double2float_rn(__ddiv_rn(x, n));
+        k[p][1] = __double2float_rn(__ddiv_rn(y, n));
+        k[p][2] = __double2float_rn(__ddiv_rn(z, n));
     }
+    kx = f2(k[0][0], k[1][0]);
+    ky = f2(k[0][1], k[1][1]);
+    kz = f2(k[0][2], k[1][2]);
+}
+
+/* Build poses g0 -> .x and g1 -> .y of the tile column S (S already offset by pp). */
+template <int NPP, int TPP>
+__device__ __forceinline__ void build_pose2(const LigView &L, const double *__restrict__ g0,
+                                            const double *__restrict__ g1, float2 *S, int sub)
+{
+    float m0[9], t0[3], m1[9], t1[3];
+    rigid_of(g0, m0, t0);
+    rigid_of(g1, m1, t1);
+    const float2 M00 = f2(m0[0], m1[0]), M01 = f2(m0[1], m1[1]), M02 = f2(m0[2], m1[2]);
+    const float2 M10 = f2(m0[3], m1[3]), M11 = f2(m0[4], m1[4]), M12 = f2(m0[5], m1[5]);
+    const float2 M20 = f2(m0[6], m1[6]), M21 = f2(m0[7], m1[7]), M22 = f2(m0[8], m1[8]);
+    const float2 TX = f2(t0[0], t1[0]), TY = f2(t0[1], t1[1]), TZ = f2(t0[2], t1[2]);
+    for (int i = sub; i < L.n_atoms; i += TPP) {
+        const float4 c = L.atom[i];
+        const float2 cx = f2(c.x), cy = f2(c.y), cz = f2(c.z);
+        VD_S2(i, 0) = add2(add2(add2(mul2(M00, cx), mul2(M01, cy)), mul2(M02, cz)), TX);
+        VD_S2(i, 1) = add2(add2(add2(mul2(M10, cx), mul2(M11, cy)), mul2(M12, cz)), TY);
+        VD_S2(i, 2) = add2(add2(add2(mul2(M20, cx), mul2(M21, cy)), mul2(M22, cz)), TZ);
+    }
+    if (TPP > 1) __syncthreads();
     for (int t = 0; t < L.n_torsions; ++t) {
-        const int4 tr = __ldg(&L.tors[t]);
-        const float ox = VD_S(tr.x, 0), oy = VD_S(tr.x, 1), oz = VD_S(tr.x, 2);
-        const double ax = (double)__fsub_rn(VD_S(tr.y, 0), ox);
-        const double ay = (double)__fsub_rn(VD_S(tr.y, 1), oy);
-        const double az = (double)__fsub_rn(VD_S(tr.y, 2), oz);
-        const double an = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)),
-                                               __dmul_rn(az, az)));
-        const float kx = __double2float_rn(__ddiv_rn(ax, an));
-        const float ky = __double2float_rn(__ddiv_rn(ay, an));
-        const float kz = __double2float_rn(__ddiv_rn(az, an));
-        double sd, cd;
-        sincos(g[7 + t], &sd, &cd);
-        const float c = __double2float_rn(cd), s = __double2float_rn(sd);
-        const float omc = __fsub_rn(1.0f, c);
-        for (int f = tr.z; f < tr.w; ++f) {
-            const int i = __ldg(&L.frag[f]);
-            const float vx = __fsub_rn(VD_S(i, 0), ox), vy = __fsub_rn(VD_S(i, 1), oy),
-                        vz = __fsub_rn(VD_S(i, 2), oz);
-            const float dot = __fadd_rn(__fadd_rn(__fmul_rn(kx, vx), __fmul_rn(ky, vy)),
-                                        __fmul_rn(kz, vz));
-            const float cxx = __fsub_rn(__fmul_rn(ky, vz), __fmul_rn(kz, vy));
-            const float cxy = __fsub_rn(__fmul_rn(kz, vx), __fmul_rn(kx, vz));
-            const float cxz = __fsub_rn(__fmul_rn(kx, vy), __fmul_rn(ky, vx));
-            const float dw = __fmul_rn(dot, omc);
-            VD_S(i, 0) = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(vx, c), __fmul_rn(cxx, s)),
-                                             __fmul_rn(kx, dw)), ox);
-            VD_S(i, 1) = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(vy, c), __fmul_rn(cxy, s)),
-                                             __fmul_rn(ky, dw)), oy);
-            VD_S(i, 2) = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(vz, c), __fmul_rn(cxz, s)),
-                                             __fmul_rn(kz, dw)), oz);
+        const int4 tr = L.tors[t];
+        const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
+        float2 KX, KY, KZ;
+        torsion_axis(sub2(VD_S2(tr.y, 0), ox), sub2(VD_S2(tr.y, 1), oy), sub2(VD_S2(tr.y, 2), oz),
+                     KX, KY, KZ);
+        double s0, c0, s1, c1;
+        sincos(g0[7 + t], &s0, &c0);
+        sincos(g1[7 + t], &s1, &c1);
+        const float2 C = f2(__double2float_rn(c0), __double2float_rn(c1));
+        const float2 SN = f2(__double2float_rn(s0), __double2float_rn(s1));
+        const float2 OMC = sub2(f2(1.0f), C);
+#pragma unroll 4
+        for (int f = tr.z + sub; f < tr.w; f += TPP) {
+            const int i = L.frag[f];
+            const float2 vx = sub2(VD_S2(i, 0), ox), vy = sub2(VD_S2(i, 1), oy),
+                         vz = sub2(VD_S2(i, 2), oz);
+            const float2 dot = add2(add2(mul2(KX, vx), mul2(KY, vy)), mul2(KZ, vz));
+            const float2 cxx = sub2(mul2(KY, vz), mul2(KZ, vy));
+            const float2 cxy = sub2(mul2(KZ, vx), mul2(KX, vz));
+            const float2 cxz = sub2(mul2(KX, vy), mul2(KY, vx));
+            const float2 dw = mul2(dot, OMC);
+            VD_S2(i, 0) = add2(add2(add2(mul2(vx, C), mul2(cxx, SN)), mul2(KX, dw)), ox);
+            VD_S2(i, 1) = add2(add2(add2(mul2(vy, C), mul2(cxy, SN)), mul2(KY, dw)), oy);
+            VD_S2(i, 2) = add2(add2(add2(mul2(vz, C), mul2(cxz, SN)), mul2(KZ, dw)), oz);
         }
+        if (TPP > 1) __syncthreads();
     }
 }
 
 /* ---- A2: inter ------------------------------------------------------------ */
+/* lerp(a, b, t) = a*(1-t) + b*t with the reference's rounding in BOTH modes:
+ * map corners reach ~1e12-5e17 next to receptor atoms, so any other lerp
+ * formulation (e.g. fma(t, b-a, a)) moves the interpolated value by more than
+ * the 1e-4 tolerance whenever the result is far smaller than its corners. */
 template <bool EXACT>
 __device__ __forceinline__ float lerp_(float a, float b, float t)
 {
-    if (EXACT) return __fadd_rn(__fmul_rn(a, __fsub_rn(1.0f, t)), __fmul_rn(b, t));
-    return fmaf(b, t, a * (1.0f - t));
+    return __fadd_rn(__fmul_rn(a, __fsub_rn(1.0f, t)), __fmul_rn(b, t));
 }
 
 template <bool EXACT>
@@ -144,59 +251,157 @@ __device__ __forceinline__ float trilerp(const float *__restrict__ m, int idx, i
     return lerp_<EXACT>(c0, c1, fz);
 }
 
-template <bool EXACT, int B>
-__device__ __forceinline__ double inter_energy(const LigView &L, const GridView &G,
-                                               const float *S)
+/* Per-atom, per-pose gather state: cell, fractions, the corner values. */
+struct Gather {
+    float fx, fy, fz, pterm;
+    bool inb;
+    float2 t[4];   /* type map z-pairs at (x,y) corners 00, 01, 10, 11 */
+    float4 ed[4];  /* elec/desolv z-pairs */
+};
+
+__device__ __forceinline__ void cell_of(const GridView &G, float x, float y, float z, float pen,
+                                        Gather &g, int &idx)
 {
-    double acc = 0.0;
-    const int nyz = G.ny * G.nz;
-    for (int i = 0; i < L.n_atoms; ++i) {
-        const float x = VD_S(i, 0), y = VD_S(i, 1), z = VD_S(i, 2);
-        float term;
-        if (x >= G.lo0 && x <= G.hi0 && y >= G.lo1 && y <= G.hi1 && z >= G.lo2 && z <= G.hi2) {
-            const float ux = __fdiv_rn(__fsub_rn(x, G.lo0), G.spacing);
-            const float uy = __fdiv_rn(__fsub_rn(y, G.lo1), G.spacing);
-            const float uz = __fdiv_rn(__fsub_rn(z, G.lo2), G.spacing);
-            const int ix = min((int)ux, G.nx - 2), iy = min((int)uy, G.ny - 2),
-                      iz = min((int)uz, G.nz - 2);
-            const float fx = __fsub_rn(ux, (float)ix), fy = __fsub_rn(uy, (float)iy),
-                        fz = __fsub_rn(uz, (float)iz);
-            const int idx = (ix * G.ny + iy) * G.nz + iz;
-            const float4 a = __ldg(&L.atom[i]);
-            const float2 a2 = __ldg(&L.atom2[i]);
-            const float vt = trilerp<EXACT>(G.maps + G.mstride * __float_as_int(a2.y), idx, G.nz,
-                                            nyz, fx, fy, fz);
-            const float ve = trilerp<EXACT>(G.maps + G.mstride * L.elec_map, idx, G.nz, nyz, fx,
-                                            fy, fz);
-            const float vd = trilerp<EXACT>(G.maps + G.mstride * L.desolv_map, idx, G.nz, nyz,
-                                            fx, fy, fz);
-            if (EXACT)
-                term = __fadd_rn(__fadd_rn(vt, __fmul_rn(a.w, ve)), __fmul_rn(a2.x, vd));
-            else
-                term = fmaf(a2.x, vd, fmaf(a.w, ve, vt));
-        } else {
-            const float dx = fmaxf(fmaxf(__fsub_rn(G.lo0, x), __fsub_rn(x, G.hi0)), 0.0f);
-            const float dy = fmaxf(fmaxf(__fsub_rn(G.lo1, y), __fsub_rn(y, G.hi1)), 0.0f);
-            const float dz = fmaxf(fmaxf(__fsub_rn(G.lo2, z), __fsub_rn(z, G.hi2)), 0.0f);
-            const float d2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)),
-                                       __fmul_rn(dz, dz));
-            term = __fmul_rn(L.penalty, __fadd_rn(__fsqrt_rn(d2), 1.0f));
-        }
-        acc = __dadd_rn(acc, (double)term);
-    }
-    return acc;
+    g.inb = x >= G.lo0 && x <= G.hi0 && y >= G.lo1 && y <= G.hi1 && z >= G.lo2 && z <= G.hi2;
+    const float dx = fmaxf(fmaxf(__fsub_rn(G.lo0, x), __fsub_rn(x, G.hi0)), 0.0f);
+    const float dy = fmaxf(fmaxf(__fsub_rn(G.lo1, y), __fsub_rn(y, G.hi1)), 0.0f);
+    const float dz = fmaxf(fmaxf(__fsub_rn(G.lo2, z), __fsub_rn(z, G.hi2)), 0.0f);
+    g.pterm = __fmul_rn(pen, __fadd_rn(
+        __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz))), 1.0f));
+    const float ux = __fdiv_rn(__fsub_rn(x, G.lo0), G.spacing);
+    const float uy = __fdiv_rn(__fsub_rn(y, G.lo1), G.spacing);
+    const float uz = __fdiv_rn(__fsub_rn(z, G.lo2), G.spacing);
+    const int ix = min(max((int)ux, 0), G.nx - 2), iy = min(max((int)uy, 0), G.ny - 2),
+              iz = min(max((int)uz, 0), G.nz - 2);
+    g.fx = __fsub_rn(ux, (float)ix);
+    g.fy = __fsub_rn(uy, (float)iy);
+    g.fz = __fsub_rn(uz, (float)iz);
+    idx = (ix * G.ny + iy) * G.nz + iz;
 }
 
-/* ---- A3: intra -------------------------------------------------------------- */
-__device__ __forceinline__ float pair_term_exact(float dx, float dy, float dz, uint32_t w,
-                                                 float4 cf, float cut2)
+__device__ __forceinline__ void issue_packed(const GridView &G, const float2 *__restrict__ tz,
+                                             int idx, Gather &g)
+{
+    const int nz = G.nz, nyz = G.ny * G.nz;
+    g.t[0] = __ldg(tz + idx);
+    g.t[1] = __ldg(tz + idx + nz);
+    g.t[2] = __ldg(tz + idx + nyz);
+    g.t[3] = __ldg(tz + idx + nyz + nz);
+    g.ed[0] = __ldg(G.ed + idx);
+    g.ed[1] = __ldg(G.ed + idx + nz);
+    g.ed[2] = __ldg(G.ed + idx + nyz);
+    g.ed[3] = __ldg(G.ed + idx + nyz + nz);
+}
+
+/* trilinear value from the 8 corners, the reference's collapse order and rounding:
+ * c(y,z) = lerp(v(0,y,z), v(1,y,z), fx); c0/c1 over y; then z. */
+__device__ __forceinline__ float tri8(float v000, float v001, float v010, float v011, float v100,
+                                      float v101, float v110, float v111, float fx, float fy,
+                                      float fz)
+{
+    const float c00 = lerp_<true>(v000, v100, fx), c10 = lerp_<true>(v010, v110, fx);
+    const float c01 = lerp_<true>(v001, v101, fx), c11 = lerp_<true>(v011, v111, fx);
+    const float c0 = lerp_<true>(c00, c10, fy), c1 = lerp_<true>(c01, c11, fy);
+    return lerp_<true>(c0, c1, fz);
+}
+
+__device__ __forceinline__ float finish_packed(const Gather &g, float q, float dsf)
+{
+    const float vt = tri8(g.t[0].x, g.t[0].y, g.t[1].x, g.t[1].y, g.t[2].x, g.t[2].y, g.t[3].x,
+                          g.t[3].y, g.fx, g.fy, g.fz);
+    const float ve = tri8(g.ed[0].x, g.ed[0].y, g.ed[1].x, g.ed[1].y, g.ed[2].x, g.ed[2].y,
+                          g.ed[3].x, g.ed[3].y, g.fx, g.fy, g.fz);
+    const float vd = tri8(g.ed[0].z, g.ed[0].w, g.ed[1].z, g.ed[1].w, g.ed[2].z, g.ed[2].w,
+                          g.ed[3].z, g.ed[3].w, g.fx, g.fy, g.fz);
+    const float gterm = __fadd_rn(__fadd_rn(vt, __fmul_rn(q, ve)), __fmul_rn(dsf, vd));
+    return g.inb ? gterm : g.pterm;
+}
+
+/* One atom of one pose against the plain (n_maps, nx, ny, nz) layout. */
+template <bool EXACT>
+__device__ __forceinline__ float atom_term(const GridView &G, const float *__restrict__ tmap,
+                                           const float *__restrict__ emap,
+                                           const float *__restrict__ dmap, float q, float dsf,
+                                           float pen, float x, float y, float z)
+{
+    Gather g;
+    int idx;
+    cell_of(G, x, y, z, pen, g, idx);
+    if (EXACT && !g.inb) return g.pterm;
+    const int nyz = G.ny * G.nz;
+    const float vt = trilerp<true>(tmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
+    const float ve = trilerp<true>(emap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
+    const float vd = trilerp<true>(dmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
+    const float gterm = __fadd_rn(__fadd_rn(vt, __fmul_rn(q, ve)), __fmul_rn(dsf, vd));
+    return g.inb ? gterm : g.pterm;
+}
+
+/* inter of both poses over this sub's atoms; EXACT requires TPP == 1 (atom order).
+ * Packed layout: software-pipelined, the gathers of atom i+TPP are in flight
+ * while atom i is interpolated. */
+template <bool EXACT, int NPP, int TPP>
+__device__ __forceinline__ void inter2(const LigView &L, const GridView &G, const float2 *S,
+                                       int sub, double &e0, double &e1)
+{
+    if (G.zp != nullptr && !EXACT) {
+        const int n = L.n_atoms;
+        int i = sub;
+        if (i >= n) return;
+        Gather c0, c1;
+        {
+            const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
+            const float2 *tz = G.zp + G.mstride * __float_as_int(L.atom2[i].y);
+            int idx0, idx1;
+            cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0);
+            cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1);
+            issue_packed(G, tz, idx0, c0);
+            issue_packed(G, tz, idx1, c1);
+        }
+        for (; i < n; i += TPP) {
+            const int in = i + TPP;
+            Gather n0, n1;
+            if (in < n) {
+                const float2 x = VD_S2(in, 0), y = VD_S2(in, 1), z = VD_S2(in, 2);
+                const float2 *tz = G.zp + G.mstride * __float_as_int(L.atom2[in].y);
+                int idx0, idx1;
+                cell_of(G, x.x, y.x, z.x, L.penalty, n0, idx0);
+                cell_of(G, x.y, y.y, z.y, L.penalty, n1, idx1);
+                issue_packed(G, tz, idx0, n0);
+                issue_packed(G, tz, idx1, n1);
+            }
+            const float q = L.atom[i].w, dsf = L.atom2[i].x;
+            e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf));
+            e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf));
+            c0 = n0;
+            c1 = n1;
+        }
+        return;
+    }
+    const float *emap = G.maps + G.mstride * L.elec_map;
+    const float *dmap = G.maps + G.mstride * L.desolv_map;
+#pragma unroll 2
+    for (int i = sub; i < L.n_atoms; i += TPP) {
+        const float4 a = L.atom[i];
+        const float2 a2 = L.atom2[i];
+        const float *tmap = G.maps + G.mstride * __float_as_int(a2.y);
+        const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
+        const float t0 = atom_term<EXACT>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.x, y.x, z.x);
+        const float t1 = atom_term<EXACT>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.y, y.y, z.y);
+        e0 = __dadd_rn(e0, (double)t0);
+        e1 = __dadd_rn(e1, (double)t1);
+    }
+}
+
+/* ---- A3: intra ---------------------------------------------------------------- */
+__device__ __forceinline__ float pair_exact(float dx, float dy, float dz, bool hb, float4 cf,
+                                            float cut2)
 {
     const float r2 = __fadd_rn(__fadd_rn(__fmul_rn(dx, dx), __fmul_rn(dy, dy)), __fmul_rn(dz, dz));
     if (r2 > cut2) return 0.0f;
     const float r2c = r2 > kMinR2 ? r2 : kMinR2;
     const float inv = __fdiv_rn(1.0f, r2c);
     const float i2 = __fmul_rn(inv, inv), i3 = __fmul_rn(i2, inv), i6 = __fmul_rn(i3, i3);
-    const float tail = (w >> 31) ? __fmul_rn(i3, i2) : i3;
+    const float tail = hb ? __fmul_rn(i3, i2) : i3;
     const float well = __fsub_rn(__fmul_rn(cf.x, i6), __fmul_rn(cf.y, tail));
     const float r = __fsqrt_rn(r2c);
     const double r64 = (double)r;
@@ -206,84 +411,232 @@ __device__ __forceinline__ float pair_term_exact(float dx, float dy, float dz, u
     return __fadd_rn(__fadd_rn(well, elec), des);
 }
 
-__device__ __forceinline__ float pair_term_fast(float dx, float dy, float dz, uint32_t w,
-                                                float4 cf, float cut2)
+/* 2^x for x <= 0 on the FMA pipe (keeps the MUFU pipe for rsqrt/ex2/rcp):
+ * n = rint(x) via the 1.5*2^23 magic add, f = x - n in [-1/2, 1/2], degree-5
+ * fit of 2^f (max rel err 3e-7), 2^n assembled in the exponent field. */
+__device__ __forceinline__ float2 exp2_poly2(float2 x)
 {
-    const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
-    const float r2c = fmaxf(r2, kMinR2);
-    const float rs = rsqrtf(r2c);                 /* MUFU.RSQ */
-    const float inv = rs * rs;                    /* 1 / r^2  */
-    const float r = r2c * rs;                     /* r        */
-    const float i2 = inv * inv, i3 = i2 * inv, i6 = i3 * i3;
-    const float tail = (w >> 31) ? i3 * i2 : i3;
-    const float well = fmaf(cf.x, i6, -cf.y * tail);
-    /* sigmoidal dielectric: eps = A + B/(1+K e),  e = exp(-lamb r)
-       elec = qq / (r eps) = qq (1 + K e) / (r (A (1 + K e) + B)) */
-    const float e1 = exp2f(r * (float)(-kLamb * 1.4426950408889634));     /* MUFU.EX2 */
-    const float den = fmaf((float)kDielK, e1, 1.0f);
-    const float elec = __fdividef(cf.z * den, r * fmaf((float)kDielA, den, (float)kDielB));
-    const float des = cf.w * exp2f(r2 * (float)(-1.4426950408889634 / kDesolvDenom)); /* MUFU.EX2 */
-    const float t = (well + elec) + des;
-    return r2 > cut2 ? 0.0f : t;
+    x = f2(fmaxf(x.x, -125.0f), fmaxf(x.y, -125.0f));
+    const float2 magic = f2(12582912.0f);
+    const float2 t = fadd2(x, magic);
+    const float2 n = fsub2(t, magic);
+    const float2 f = fsub2(x, n);
+    float2 p = fma2(f2(0.0012979109305888414f), f, f2(0.009670717641711235f));
+    p = fma2(p, f, f2(0.055515434592962265f));
+    p = fma2(p, f, f2(0.24022223055362701f));
+    p = fma2(p, f, f2(0.6931465268135071f));
+    p = fma2(p, f, f2(1.0f));
+    const float2 sc = f2(__int_as_float((__float_as_int(t.x) << 23) + 0x3f800000),
+                         __int_as_float((__float_as_int(t.y) << 23) + 0x3f800000));
+    return fmul2(p, sc);
 }
 
-template <bool EXACT, int B>
-__device__ __forceinline__ double intra_energy(const LigView &L, const float *S)
+/* FAST pair term for two poses (packed f32x2; MUFU for rsqrt/exp2/rcp).
+ *   eps(r) = A + B/(1+K e), e = exp(-lamb r)  =>  elec = qq (1+K e) / (r (A (1+K e) + B)) */
+template <bool HB, bool CUT>
+__device__ __forceinline__ float2 pair_fast2(float2 dx, float2 dy, float2 dz, float4 cf, float cut2)
 {
-    const int n = L.n_pairs;
-    if (EXACT) {
-        /* simd lane-blocked order, lane = 8 (scoring/simd.py:58-86) */
-        double lane[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const int nblk = n >> 3;
-        for (int blk = 0; blk < nblk; ++blk) {
-#pragma unroll
-            for (int l = 0; l < 8; ++l) {
-                const int k = blk * 8 + l;
-                const uint32_t w = __ldg(&L.pij[k]);
-                const float4 cf = __ldg(&L.pcoef[k]);
-                const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
-                const float t = pair_term_exact(__fsub_rn(VD_S(i, 0), VD_S(j, 0)),
-                                                __fsub_rn(VD_S(i, 1), VD_S(j, 1)),
-                                                __fsub_rn(VD_S(i, 2), VD_S(j, 2)), w, cf, L.cut2);
-                lane[l] = __dadd_rn(lane[l], (double)t);
-            }
-        }
-        double tail = 0.0;
-        for (int k = nblk * 8; k < n; ++k) {
-            const uint32_t w = __ldg(&L.pij[k]);
-            const float4 cf = __ldg(&L.pcoef[k]);
-            const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
-            tail = __dadd_rn(tail, (double)pair_term_exact(__fsub_rn(VD_S(i, 0), VD_S(j, 0)),
-                                                           __fsub_rn(VD_S(i, 1), VD_S(j, 1)),
-                                                           __fsub_rn(VD_S(i, 2), VD_S(j, 2)), w,
-                                                           cf, L.cut2));
-        }
-        double tot = 0.0;
-#pragma unroll
-        for (int l = 0; l < 8; ++l) tot = __dadd_rn(tot, lane[l]);
-        return __dadd_rn(tot, tail);
-    } else {
-        double acc = 0.0;
-        for (int k0 = 0; k0 < n; k0 += 32) {
-            const int k1 = min(k0 + 32, n);
-            float part = 0.0f;
+    const float2 r2 = fma2(dz, dz, fma2(dy, dy, fmul2(dx, dx)));
+    const float2 r2c = f2(fmaxf(r2.x, kMinR2), fmaxf(r2.y, kMinR2));
+    const float2 rs = f2(mufu_rsq(r2c.x), mufu_rsq(r2c.y));
+    const float2 inv = fmul2(rs, rs);
+    const float2 r = fmul2(r2c, rs);
+    const float2 i2 = fmul2(inv, inv);
+    const float2 i3 = fmul2(i2, inv);
+    const float2 i6 = fmul2(i3, i3);
+    const float2 tail = HB ? fmul2(i3, i2) : i3;
+    const float2 well = fma2(f2(cf.x), i6, fmul2(f2(-cf.y), tail));
+    const float2 earg = fmul2(r, f2((float)(-kLamb * 1.4426950408889634)));
+    const float2 e = f2(mufu_ex2(earg.x), mufu_ex2(earg.y));
+    const float2 den = fma2(f2((float)kDielK), e, f2(1.0f));
+    const float2 dd = fmul2(r, fma2(f2((float)kDielA), den, f2((float)kDielB)));
+    const float2 rc = f2(mufu_rcp(dd.x), mufu_rcp(dd.y));
+    const float2 elec = fmul2(fmul2(f2(cf.z), den), rc);
+    const float2 darg = fmul2(r2, f2((float)(-1.4426950408889634 / kDesolvDenom)));
+    const float2 des = fmul2(f2(cf.w), exp2_poly2(darg));
+    float2 t = fadd2(fadd2(well, elec), des);
+    if (CUT) {
+        t.x = r2.x > cut2 ? 0.0f : t.x;
+        t.y = r2.y > cut2 ? 0.0f : t.y;
+    }
+    return t;
+}
+
+template <int NPP, int TPP, bool HB, bool CUT>
+__device__ __forceinline__ float2 row_fast(const float2 *S, int i, int kb, int ke,
+                                           const float4 *tc, const int *tj, int sub, float cut2)
+{
+    const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
+    float2 acc = f2(0.0f);
 #pragma unroll 4
-            for (int k = k0; k < k1; ++k) {
-                const uint32_t w = __ldg(&L.pij[k]);
-                const float4 cf = __ldg(&L.pcoef[k]);
-                const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
-                part += pair_term_fast(VD_S(i, 0) - VD_S(j, 0), VD_S(i, 1) - VD_S(j, 1),
-                                       VD_S(i, 2) - VD_S(j, 2), w, cf, L.cut2);
+    for (int k = kb + sub; k < ke; k += TPP) {
+        const float4 c = tc[k];
+        const int j = tj[k];
+        acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(xi, VD_S2(j, 0)), fsub2(yi, VD_S2(j, 1)),
+                                            fsub2(zi, VD_S2(j, 2)), c, cut2));
+    }
+    return acc;
+}
+
+/* Shared-memory pair staging area (per CTA). */
+struct PairTile {
+    float4 *coef;   /* [kTile] */
+    int *j;         /* [kTile] fast: j; exact: packed ij */
+    int4 *row;      /* [kTile] fast rows of the tile */
+};
+
+/* intra of both poses over this sub's share of the pairs (all CTA threads must call) */
+template <bool EXACT, int NPP, int TPP>
+__device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const PairTile &T,
+                                       int sub, double &a0, double &a1)
+{
+    const int n = L.n_pairs, B = NPP * TPP, tid = threadIdx.x;
+    if (n == 0) return;
+    if (EXACT) {
+        /* reference lane-8 order (scoring/simd.py:58-86): lane[k & 7] over the
+           first 8*floor(n/8) pairs, then a sequential tail, then lanes 0..7 + tail */
+        double l0[8], l1[8], tail0 = 0.0, tail1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) l0[l] = l1[l] = 0.0;
+        const int nblk8 = n & ~7;
+        for (int k0 = 0; k0 < n; k0 += kTile) {
+            const int cnt = min(kTile, n - k0);
+            __syncthreads();
+            for (int k = tid; k < cnt; k += B) {
+                T.coef[k] = __ldg(&L.pcoef[k0 + k]);
+                T.j[k] = (int)__ldg(&L.pij[k0 + k]);
             }
-            acc += (double)part;
+            __syncthreads();
+            const int cb = min(cnt, max(0, nblk8 - k0));  /* lane-blocked part of this tile */
+            for (int kb = 0; kb < cb; kb += 8) {
+#pragma unroll
+                for (int l = 0; l < 8; ++l) {
+                    const uint32_t w = (uint32_t)T.j[kb + l];
+                    const float4 c = T.coef[kb + l];
+                    const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
+                    const bool hb = w >> 31;
+                    const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
+                    const float2 xj = VD_S2(j, 0), yj = VD_S2(j, 1), zj = VD_S2(j, 2);
+                    l0[l] = __dadd_rn(l0[l], (double)pair_exact(__fsub_rn(xi.x, xj.x), __fsub_rn(yi.x, yj.x),
+                                                                __fsub_rn(zi.x, zj.x), hb, c, L.cut2));
+                    l1[l] = __dadd_rn(l1[l], (double)pair_exact(__fsub_rn(xi.y, xj.y), __fsub_rn(yi.y, yj.y),
+                                                                __fsub_rn(zi.y, zj.y), hb, c, L.cut2));
+                }
+            }
+            for (int k = cb; k < cnt; ++k) {
+                const uint32_t w = (uint32_t)T.j[k];
+                const float4 c = T.coef[k];
+                const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
+                const bool hb = w >> 31;
+                const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
+                const float2 xj = VD_S2(j, 0), yj = VD_S2(j, 1), zj = VD_S2(j, 2);
+                tail0 = __dadd_rn(tail0, (double)pair_exact(__fsub_rn(xi.x, xj.x), __fsub_rn(yi.x, yj.x),
+                                                            __fsub_rn(zi.x, zj.x), hb, c, L.cut2));
+                tail1 = __dadd_rn(tail1, (double)pair_exact(__fsub_rn(xi.y, xj.y), __fsub_rn(yi.y, yj.y),
+                                                            __fsub_rn(zi.y, zj.y), hb, c, L.cut2));
+            }
         }
-        return acc;
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            s0 = __dadd_rn(s0, l0[l]);
+            s1 = __dadd_rn(s1, l1[l]);
+        }
+        a0 = __dadd_rn(s0, tail0);
+        a1 = __dadd_rn(s1, tail1);
+    } else {
+        const bool cut = L.cut2 < INFINITY;
+        double s0 = 0.0, s1 = 0.0;
+        int t = 0;
+        for (int k0 = 0; k0 < n; k0 += kTile, ++t) {
+            const int cnt = min(kTile, n - k0);
+            const int r0 = __ldg(&L.ftile[t]), r1 = __ldg(&L.ftile[t + 1]);
+            __syncthreads();
+            for (int k = tid; k < cnt; k += B) {
+                T.coef[k] = __ldg(&L.fcoef[k0 + k]);
+                T.j[k] = __ldg(&L.fj[k0 + k]);
+            }
+            for (int r = tid; r < r1 - r0; r += B) T.row[r] = __ldg(&L.frow[r0 + r]);
+            __syncthreads();
+            float2 part = f2(0.0f);
+            for (int r = 0; r < r1 - r0; ++r) {
+                const int4 row = T.row[r];
+                const int kb = row.y - k0, ke = row.z - k0;
+                float2 v;
+                if (row.w) v = cut ? row_fast<NPP, TPP, true, true>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2)
+                                   : row_fast<NPP, TPP, true, false>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2);
+                else v = cut ? row_fast<NPP, TPP, false, true>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2)
+                             : row_fast<NPP, TPP, false, false>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2);
+                part = fadd2(part, v);
+            }
+            s0 += (double)part.x;
+            s1 += (double)part.y;
+        }
+        a0 = s0;
+        a1 = s1;
     }
 }
 
 __device__ __forceinline__ float total32(double inter, double intra, float tors)
 {
     return __fadd_rn(__fadd_rn(__double2float_rn(inter), __double2float_rn(intra)), tors);
+}
+
+/* Sum per-sub partials (fast mode, TPP > 1) into sub 0; red: double[4][TPP][NPP]. */
+template <int NPP, int TPP>
+__device__ __forceinline__ void reduce_subs(double *red, int pp, int sub, double &e0, double &e1,
+                                            double &a0, double &a1)
+{
+    if (TPP == 1) return;
+    __syncthreads();
+    red[(0 * TPP + sub) * NPP + pp] = e0;
+    red[(1 * TPP + sub) * NPP + pp] = e1;
+    red[(2 * TPP + sub) * NPP + pp] = a0;
+    red[(3 * TPP + sub) * NPP + pp] = a1;
+    __syncthreads();
+    if (sub == 0) {
+#pragma unroll
+        for (int s = 1; s < TPP; ++s) {
+            e0 += red[(0 * TPP + s) * NPP + pp];
+            e1 += red[(1 * TPP + s) * NPP + pp];
+            a0 += red[(2 * TPP + s) * NPP + pp];
+            a1 += red[(3 * TPP + s) * NPP + pp];
+        }
+    }
+}
+
+/* Dynamic shared-memory layout of the scoring CTAs. */
+struct SmemLayout {
+    unsigned topo_atom, topo_atom2, topo_tors, topo_frag;
+    unsigned tile_coef, tile_j, tile_row, red, extra, bytes;
+};
+
+__host__ __device__ inline unsigned align16(unsigned v) { return (v + 15u) & ~15u; }
+
+__host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n_frag, int npp,
+                                                  int tpp, unsigned extra)
+{
+    SmemLayout s;
+    unsigned off = align16(8u * 3u * (unsigned)n_atoms * (unsigned)npp);
+    s.topo_atom = off;
+    off = align16(off + 16u * (unsigned)n_atoms);
+    s.topo_atom2 = off;
+    off = align16(off + 8u * (unsigned)n_atoms);
+    s.topo_tors = off;
+    off = align16(off + 16u * (unsigned)n_tors);
+    s.topo_frag = off;
+    off = align16(off + 4u * (unsigned)n_frag);
+    s.tile_coef = off;
+    off += 16u * kTile;
+    s.tile_row = off;
+    off += 16u * kTile;
+    s.tile_j = off;
+    off += 4u * kTile;
+    s.red = off;
+    off += (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
+    s.extra = align16(off);
+    s.bytes = align16(s.extra + extra);
+    return s;
 }
 
 }  // namespace vd

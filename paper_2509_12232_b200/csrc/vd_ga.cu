@@ -138,18 +138,25 @@ __device__ void breed_child(const GaDev &P, int G, const double *cur, const floa
 }
 
 struct GaLayout {
-    int nmax;                 /* atoms of the largest ligand: pose tile is [3][nmax][B] f32 */
-    unsigned off_fit, off_e, off_a, off_taken, bytes;
+    SmemLayout base;          /* pose tile + pair tiles (+ reduction) for the largest ligand */
+    unsigned off_fit, off_e, off_a, off_taken;
 };
 
-template <bool EXACT, int B>
-__global__ void __launch_bounds__(B) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
-                                               const int *__restrict__ order, int count, GaDev P,
-                                               uint64_t seed, int64_t base, int *work,
-                                               double *gene_buf, int gmax, GaLayout lay, GaOut out)
+template <bool EXACT, int NPP, int TPP>
+__global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+                                                      const int *__restrict__ order, int count,
+                                                      GaDev P, uint64_t seed, int64_t base,
+                                                      int *work, double *gene_buf, int gmax,
+                                                      GaLayout lay, GaOut out)
 {
+    constexpr int B = NPP * TPP;
     extern __shared__ __align__(16) unsigned char smem[];
-    float *S = reinterpret_cast<float *>(smem) + threadIdx.x;
+    const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
+    float2 *S = reinterpret_cast<float2 *>(smem) + pp;
+    PairTile Tl{reinterpret_cast<float4 *>(smem + lay.base.tile_coef),
+                reinterpret_cast<int *>(smem + lay.base.tile_j),
+                reinterpret_cast<int4 *>(smem + lay.base.tile_row)};
+    double *red = reinterpret_cast<double *>(smem + lay.base.red);
     float *fit = reinterpret_cast<float *>(smem + lay.off_fit);
     double *e64 = reinterpret_cast<double *>(smem + lay.off_e);
     double *a64 = reinterpret_cast<double *>(smem + lay.off_a);
@@ -167,7 +174,8 @@ __global__ void __launch_bounds__(B) ga_kernel(GridView Gv, const LigView *__res
         __syncthreads();
         if (slot >= count) break;
         const int l = order ? order[slot] : slot;
-        const LigView L = ligs[l];
+        const LigView L = stage_topology(ligs[l], smem, lay.base.topo_atom, lay.base.topo_atom2,
+                                         lay.base.topo_tors, lay.base.topo_frag);
         const int T = L.n_torsions, G = 7 + T;
         const uint64_t k0 = seed, k1 = (uint64_t)(base + l);
         double *cur = buf0, *nxt = buf1;
@@ -176,13 +184,18 @@ __global__ void __launch_bounds__(B) ga_kernel(GridView Gv, const LigView *__res
         bool have = false;
         __syncthreads();
         for (int gen = 0; gen <= P.generations; ++gen) {
-            for (int i = threadIdx.x; i < pop; i += B) {
-                build_pose<B>(L, cur + (size_t)i * G, S);
-                const double e = inter_energy<EXACT, B>(L, Gv, S);
-                const double a = L.n_pairs ? intra_energy<EXACT, B>(L, S) : 0.0;
-                e64[i] = e;
-                a64[i] = a;
-                fit[i] = total32(e, a, L.tors32);
+            for (int b0 = 0; b0 < pop; b0 += 2 * NPP) {
+                const int i0 = b0 + 2 * pp, i1 = i0 + 1;
+                const int q0 = min(i0, pop - 1), q1 = min(i1, pop - 1);
+                build_pose2<NPP, TPP>(L, cur + (size_t)q0 * G, cur + (size_t)q1 * G, S, sub);
+                double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
+                inter2<EXACT, NPP, TPP>(L, Gv, S, sub, e0, e1);
+                intra2<EXACT, NPP, TPP>(L, S, Tl, sub, a0, a1);
+                reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
+                if (sub == 0) {
+                    if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
+                    if (i1 < pop) { e64[i1] = e1; a64[i1] = a1; fit[i1] = total32(e1, a1, L.tors32); }
+                }
             }
             __syncthreads();
             const int idx = block_argmin(fit, nullptr, pop, s_idx, s_val);
@@ -220,47 +233,46 @@ __global__ void __launch_bounds__(B) ga_kernel(GridView Gv, const LigView *__res
     }
 }
 
-template <bool EXACT, int B>
+template <bool EXACT, int NPP, int TPP>
 static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
-                               int count, const GaDev &P, uint64_t seed, int64_t base,
-                               double *gene_buf_dummy, int gmax, const GaLayout &lay,
-                               const GaOut &out, cudaStream_t st, int *d_work, double **gene_buf,
-                               int *n_ctas)
+                               int count, const GaDev &P, uint64_t seed, int64_t base, int gmax,
+                               const GaLayout &lay, const GaOut &out, cudaStream_t st,
+                               int *d_work, double **gene_buf, int *n_ctas)
 {
-    (void)gene_buf_dummy;
-    auto k = ga_kernel<EXACT, B>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+    auto k = ga_kernel<EXACT, NPP, TPP>;
+    const unsigned bytes = lay.base.bytes;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 0, dev = 0, sms = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, B, lay.bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NPP * TPP, bytes);
     if (e != cudaSuccess) return e;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int ctas = std::max(1, std::min(count, std::max(1, per_sm) * sms));
     e = cudaMallocAsync((void **)gene_buf, sizeof(double) * (size_t)ctas * 2 * P.pop * gmax, st);
     if (e != cudaSuccess) return e;
-    k<<<ctas, B, lay.bytes, st>>>(Gv, d_ligs, d_order, count, P, seed, base, d_work, *gene_buf, gmax, lay, out);
+    k<<<ctas, NPP * TPP, bytes, st>>>(Gv, d_ligs, d_order, count, P, seed, base, d_work, *gene_buf,
+                                      gmax, lay, out);
     ++vdi::g_launches;
     *n_ctas = ctas;
     return cudaGetLastError();
 }
 
-cudaError_t launch_ga(int mode, int B, const GridView &Gv, const LigView *d_ligs,
+cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const LigView *d_ligs,
                       const int *d_order, int count, const GaDev &P, uint64_t seed, int64_t base,
                       int gmax, const GaLayout &lay, const GaOut &out, cudaStream_t st,
                       int *d_work, double **gene_buf, int *n_ctas)
 {
-#define VD_GA_CASE(EX, BB) \
-    return launch_ga_t<EX, BB>(Gv, d_ligs, d_order, count, P, seed, base, nullptr, gmax, lay, out, st, d_work, gene_buf, n_ctas)
-    if (mode == VD_MODE_EXACT) {
-        if (B == 128) VD_GA_CASE(true, 128);
-        if (B == 64) VD_GA_CASE(true, 64);
-        VD_GA_CASE(true, 32);
-    }
-    if (B == 128) VD_GA_CASE(false, 128);
-    if (B == 64) VD_GA_CASE(false, 64);
-    VD_GA_CASE(false, 32);
-#undef VD_GA_CASE
+#define VD_G(EX, N, T)                                                                             \
+    if (exact == EX && npp == N && tpp == T)                                                       \
+    return launch_ga_t<EX, N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, st,   \
+                                 d_work, gene_buf, n_ctas)
+    VD_G(true, 64, 1); VD_G(true, 32, 1); VD_G(true, 16, 1);
+    VD_G(false, 64, 1); VD_G(false, 32, 1); VD_G(false, 16, 1);
+    VD_G(false, 64, 2); VD_G(false, 32, 2); VD_G(false, 16, 2);
+    VD_G(false, 64, 4); VD_G(false, 32, 4); VD_G(false, 16, 4);
+#undef VD_G
+    return cudaErrorInvalidConfiguration;
 }
 
 }  // namespace vd
@@ -287,11 +299,12 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     /* ligand views + largest-first order */
     std::vector<vd::LigView> views(count);
     std::vector<int> order(count);
-    int nmax = 1, tmax = 0;
+    int nmax = 1, tmax = 0, fmax = 0;
     for (int l = 0; l < count; ++l) {
         views[l] = s->view(first + l);
         nmax = std::max(nmax, views[l].n_atoms);
         tmax = std::max(tmax, views[l].n_torsions);
+        fmax = std::max(fmax, views[l].n_frag);
         order[l] = l;
     }
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
@@ -304,26 +317,28 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         set_error("vd_dock_batch: gstride smaller than 7 + max torsions");
         return -1;
     }
-    int B;
-    if (vdi::pick_block(nmax, &B)) return -1;
+    const bool exact = mode == VD_MODE_EXACT;
+    int npp, tpp;
+    if (vd::pick_shape(nmax, exact, &npp, &tpp)) return -1;
     vd::GaLayout lay;
-    lay.nmax = nmax;
-    unsigned off = (unsigned)(sizeof(float) * 3 * (size_t)nmax * B);
-    off = (off + 15) & ~15u;
-    lay.off_fit = off;
-    off += sizeof(float) * p->pop;
-    off = (off + 15) & ~15u;
-    lay.off_e = off;
-    off += sizeof(double) * p->pop;
-    lay.off_a = off;
-    off += sizeof(double) * p->pop;
-    lay.off_taken = off;
-    off += p->pop;
-    lay.bytes = (off + 15) & ~15u;
-    if (lay.bytes > 227 * 1024) {
+    const unsigned extra = (unsigned)p->pop * (4u + 8u + 8u + 1u) + 64u;
+    for (;;) {
+        lay.base = vd::smem_layout(nmax, tmax, fmax, npp, tpp, extra);
+        if (lay.base.bytes <= 227u * 1024u || npp == 16) break;
+        npp /= 2;
+    }
+    if (lay.base.bytes > 227u * 1024u) {
         set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
         return -1;
     }
+    unsigned off = lay.base.extra;
+    lay.off_e = off;
+    off += 8u * p->pop;
+    lay.off_a = off;
+    off += 8u * p->pop;
+    lay.off_fit = off;
+    off += 4u * p->pop;
+    lay.off_taken = off;
     vd::GaDev P;
     P.pop = p->pop; P.generations = p->generations; P.tournament = p->tournament;
     P.elitism = p->elitism;
@@ -358,7 +373,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     o.best_total = d_bt; o.best_inter = d_be; o.best_intra = d_ba; o.best_genes = d_bg;
     o.gstride = gstride; o.trace = d_tr; o.n_evals = d_ne;
     int n_ctas = 0;
-    VD_CK(vd::launch_ga(mode, B, vdi::grid_view(g), d_views, d_order, count, P, seed,
+    VD_CK(vd::launch_ga(exact, npp, tpp, vdi::grid_view(g, s->elec_map, s->desolv_map), d_views, d_order, count, P, seed,
                         lig_index_base, gmax, lay, o, st, d_work, &gene_buf, &n_ctas));
     if (!dev_out) {
         VD_CK(cudaMemcpyAsync(best_total, d_bt, sizeof(float) * count, cudaMemcpyDeviceToHost, st));

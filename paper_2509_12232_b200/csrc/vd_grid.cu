@@ -209,7 +209,7 @@ extern "C" int vd_grid_build(const float *rec_xyz, const int32_t *rec_type, cons
         vd::grid_kernel<<<(unsigned)((n_nodes + vd::kGridTile - 1) / vd::kGridTile), vd::kGridTile>>>(a);
         ++vdi::g_launches;
         ok = vdi::check(cudaGetLastError(), "grid kernel") &&
-             vdi::check(cudaDeviceSynchronize(), "grid kernel sync");
+             vdi::check(cudaDeviceSynchronize(), "grid kernel sync") && vdi::make_packed(g);
     }
     cudaFree(d_rec);
     cudaFree(d_rt);

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -14,6 +16,9 @@ struct vd_grid {
     int n_maps, nx, ny, nz;
     float lo[3], hi[3], spacing;
     float *d_maps;           /* (n_maps, nx, ny, nz) */
+    float2 *d_zp;            /* packed z-pairs of every map, or null (see GridView) */
+    std::mutex ed_lock;
+    std::map<std::pair<int, int>, float4 *> d_ed;  /* packed (elec, desolv) per map pair */
 };
 
 struct vd_ligands {
@@ -29,6 +34,11 @@ struct vd_ligands {
     float4 *d_pcoef;
     int4 *d_tors;
     int *d_frag;
+    float4 *d_fcoef;          /* fast-order pairs */
+    int *d_fj;
+    int4 *d_frow;
+    int *d_ftile;
+    std::vector<int> frow_start, ftile_start, n_frag;  /* per-ligand offsets into d_frow / d_ftile */
     vd::LigView view(int lig) const;
 };
 
@@ -37,9 +47,14 @@ void set_error(const std::string &msg);
 bool check(cudaError_t e, const char *what);
 bool is_device_ptr(const void *p);
 extern thread_local int64_t g_launches;
-vd::GridView grid_view(const vd_grid *g);
-int pick_block(int n_atoms, int *block);  /* poses per CTA for an atom count */
+vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map);
+bool make_packed(vd_grid *g);
+
 }  // namespace vdi
+
+namespace vd {
+int pick_shape(int n_atoms, bool exact, int *npp, int *tpp);
+}
 
 #define VD_CK(call)                                        \
     do {                                                   \

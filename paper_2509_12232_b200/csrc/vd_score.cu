@@ -1,129 +1,166 @@
 /*
- * vd_score.cu -- fused pose + inter + intra scoring kernels (thread per pose).
+ * vd_score.cu -- fused pose + inter + intra scoring kernel.
  *
  * One launch scores P genotypes (or given poses) of ONE ligand:
  * SimdBackend.dock_population / score_many semantics
  * (vd/scoring/simd.py:141-154, 225-240, 277-311) plus the total32 rounding of
- * vd/scoring/__init__.py:345.  See vd_device.cuh for the stage contracts.
+ * vd/scoring/__init__.py:345.  A CTA owns 2*NPP poses (NPP pose pairs, TPP
+ * threads per pair); see vd_device.cuh for the stage contracts.
  */
+#include <cstdlib>
+
 #include "vd_internal.h"
 
 namespace vd {
 
-enum { SRC_GENES = 0, SRC_POSES = 1 };
-
-template <bool EXACT, int B, int SRC>
-__global__ void __launch_bounds__(B) score_kernel(GridView G, LigView L,
-                                                  const double *__restrict__ genes,
-                                                  const float *__restrict__ poses, int64_t P,
-                                                  int ngenes, double *__restrict__ inter,
-                                                  double *__restrict__ intra,
-                                                  float *__restrict__ total)
+template <bool EXACT, int NPP, int TPP>
+__global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
+                                                         const double *__restrict__ genes,
+                                                         const float *__restrict__ poses,
+                                                         int64_t P, int ngenes, SmemLayout lay,
+                                                         double *__restrict__ inter,
+                                                         double *__restrict__ intra,
+                                                         float *__restrict__ total)
 {
-    extern __shared__ float smem[];
-    const int64_t p = (int64_t)blockIdx.x * B + threadIdx.x;
-    if (p >= P) return;
-    float *S = smem + threadIdx.x;
-    if (SRC == SRC_GENES) {
-        build_pose<B>(L, genes + p * ngenes, S);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
+    float2 *S = reinterpret_cast<float2 *>(smem) + pp;
+    PairTile T{reinterpret_cast<float4 *>(smem + lay.tile_coef),
+               reinterpret_cast<int *>(smem + lay.tile_j),
+               reinterpret_cast<int4 *>(smem + lay.tile_row)};
+    const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
+                                     lay.topo_frag);
+    __syncthreads();
+    const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
+    const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;  /* tail: duplicate, drop */
+    if (genes) {
+        build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub);
     } else {
-        const float *src = poses + p * 3 * L.n_atoms;
-        for (int i = 0; i < L.n_atoms; ++i) {
-            VD_S(i, 0) = src[i];
-            VD_S(i, 1) = src[L.n_atoms + i];
-            VD_S(i, 2) = src[2 * L.n_atoms + i];
+        const int n = L.n_atoms;
+        const float *s0 = poses + q0 * 3 * n, *s1 = poses + q1 * 3 * n;
+        for (int i = sub; i < n; i += TPP)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) VD_S2(i, c) = f2(s0[c * n + i], s1[c * n + i]);
+        if (TPP > 1) __syncthreads();
+    }
+    double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
+    inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
+    intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
+    reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
+    if (sub == 0) {
+        if (p0 < P) {
+            inter[p0] = e0;
+            intra[p0] = a0;
+            if (total) total[p0] = total32(e0, a0, L.tors32);
+        }
+        if (p1 < P) {
+            inter[p1] = e1;
+            intra[p1] = a1;
+            if (total) total[p1] = total32(e1, a1, L.tors32);
         }
     }
-    const double e = inter_energy<EXACT, B>(L, G, S);
-    const double a = L.n_pairs ? intra_energy<EXACT, B>(L, S) : 0.0;
-    inter[p] = e;
-    intra[p] = a;
-    if (total) total[p] = total32(e, a, L.tors32);
 }
 
-template <int B>
-__global__ void __launch_bounds__(B) pose_kernel(LigView L, const double *__restrict__ genes,
-                                                 int64_t P, int ngenes, float *__restrict__ out)
+template <int NPP>
+__global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__restrict__ genes,
+                                                   int64_t P, int ngenes, SmemLayout lay,
+                                                   float *__restrict__ out)
 {
-    extern __shared__ float smem[];
-    const int64_t p = (int64_t)blockIdx.x * B + threadIdx.x;
-    if (p >= P) return;
-    float *S = smem + threadIdx.x;
-    build_pose<B>(L, genes + p * ngenes, S);
-    float *dst = out + p * 3 * L.n_atoms;
-    for (int i = 0; i < L.n_atoms; ++i) {
-        dst[i] = VD_S(i, 0);
-        dst[L.n_atoms + i] = VD_S(i, 1);
-        dst[2 * L.n_atoms + i] = VD_S(i, 2);
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int pp = threadIdx.x;
+    const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
+                                     lay.topo_frag);
+    __syncthreads();
+    float2 *S = reinterpret_cast<float2 *>(smem) + pp;
+    const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
+    const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;
+    build_pose2<NPP, 1>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, 0);
+    const int n = L.n_atoms;
+    for (int i = 0; i < n; ++i)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float2 v = VD_S2(i, c);
+            if (p0 < P) out[(p0 * 3 + c) * n + i] = v.x;
+            if (p1 < P) out[(p1 * 3 + c) * n + i] = v.y;
+        }
+}
+
+/* Launch shape for a ligand: pose pairs per CTA (NPP) and threads per pair (TPP). */
+int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
+{
+    const unsigned limit = 200 * 1024;
+    int t = exact ? 1 : (n_atoms <= 40 ? 1 : (n_atoms <= 80 ? 2 : 4));
+    if (!exact)
+        if (const char *ov = getenv("VD_TPP")) {  /* tuning override: 1, 2 or 4 */
+            const int v = atoi(ov);
+            if (v == 1 || v == 2 || v == 4) t = v;
+        }
+    for (int n : {64, 32, 16}) {
+        if (smem_layout(n_atoms, 64, 4 * n_atoms, n, t, 0).bytes <= limit) {
+            *npp = n;
+            *tpp = t;
+            return 0;
+        }
     }
+    vdi::set_error("ligand too large for the shared-memory pose tile (n_atoms = " +
+                   std::to_string(n_atoms) + ")");
+    return -1;
 }
 
-template <bool EXACT, int B, int SRC>
-static cudaError_t launch_score_t(const GridView &G, const LigView &L, const double *genes,
-                                  const float *poses, int64_t P, int ngenes, double *inter,
-                                  double *intra, float *total, cudaStream_t st)
+template <bool EXACT, int NPP, int TPP>
+static cudaError_t launch_t(const GridView &G, const LigView &L, const double *genes,
+                            const float *poses, int64_t P, int ngenes, double *inter,
+                            double *intra, float *total, cudaStream_t st)
 {
-    const size_t smem = sizeof(float) * 3 * (size_t)L.n_atoms * B;
-    auto k = score_kernel<EXACT, B, SRC>;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0);
+    auto k = score_kernel<EXACT, NPP, TPP>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
     if (e != cudaSuccess) return e;
-    const int64_t blocks = (P + B - 1) / B;
-    k<<<(unsigned)blocks, B, smem, st>>>(G, L, genes, poses, P, ngenes, inter, intra, total);
+    const int64_t per_cta = 2 * NPP;
+    const int64_t blocks = (P + per_cta - 1) / per_cta;
+    k<<<(unsigned)blocks, NPP * TPP, lay.bytes, st>>>(G, L, genes, poses, P, ngenes, lay, inter,
+                                                        intra, total);
     ++vdi::g_launches;
     return cudaGetLastError();
-}
-
-template <bool EXACT, int SRC>
-static cudaError_t launch_score_m(int B, const GridView &G, const LigView &L, const double *genes,
-                                  const float *poses, int64_t P, int ngenes, double *inter,
-                                  double *intra, float *total, cudaStream_t st)
-{
-    switch (B) {
-    case 128: return launch_score_t<EXACT, 128, SRC>(G, L, genes, poses, P, ngenes, inter, intra, total, st);
-    case 64: return launch_score_t<EXACT, 64, SRC>(G, L, genes, poses, P, ngenes, inter, intra, total, st);
-    default: return launch_score_t<EXACT, 32, SRC>(G, L, genes, poses, P, ngenes, inter, intra, total, st);
-    }
 }
 
 cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
                          const double *genes, const float *poses, int64_t P, int ngenes,
                          double *inter, double *intra, float *total, cudaStream_t st)
 {
-    int B;
-    if (vdi::pick_block(L.n_atoms, &B)) return cudaErrorInvalidValue;
+    const bool exact = mode == VD_MODE_EXACT;
+    int npp, tpp;
+    if (pick_shape(L.n_atoms, exact, &npp, &tpp)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
-    if (mode == VD_MODE_EXACT)
-        return src == SRC_GENES
-                   ? launch_score_m<true, SRC_GENES>(B, G, L, genes, poses, P, ngenes, inter, intra, total, st)
-                   : launch_score_m<true, SRC_POSES>(B, G, L, genes, poses, P, ngenes, inter, intra, total, st);
-    return src == SRC_GENES
-               ? launch_score_m<false, SRC_GENES>(B, G, L, genes, poses, P, ngenes, inter, intra, total, st)
-               : launch_score_m<false, SRC_POSES>(B, G, L, genes, poses, P, ngenes, inter, intra, total, st);
+    const double *g = src == 0 ? genes : nullptr;
+    const float *p = src == 0 ? nullptr : poses;
+#define VD_L(EX, N, T) \
+    if (exact == EX && npp == N && tpp == T) return launch_t<EX, N, T>(G, L, g, p, P, ngenes, inter, intra, total, st)
+    VD_L(true, 64, 1); VD_L(true, 32, 1); VD_L(true, 16, 1);
+    VD_L(false, 64, 1); VD_L(false, 32, 1); VD_L(false, 16, 1);
+    VD_L(false, 64, 2); VD_L(false, 32, 2); VD_L(false, 16, 2);
+    VD_L(false, 64, 4); VD_L(false, 32, 4); VD_L(false, 16, 4);
+#undef VD_L
+    return cudaErrorInvalidConfiguration;
 }
 
 cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ngenes, float *out,
                         cudaStream_t st)
 {
-    int B;
-    if (vdi::pick_block(L.n_atoms, &B)) return cudaErrorInvalidValue;
+    int npp, tpp;
+    if (pick_shape(L.n_atoms, true, &npp, &tpp)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
-    const size_t smem = sizeof(float) * 3 * (size_t)L.n_atoms * B;
-    const int64_t blocks = (P + B - 1) / B;
+    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, 1, 0);
+    const size_t smem = lay.bytes;
+    const int64_t blocks = (P + 2 * npp - 1) / (2 * npp);
     cudaError_t e;
-    switch (B) {
-    case 128:
-        e = cudaFuncSetAttribute(pose_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) pose_kernel<128><<<(unsigned)blocks, 128, smem, st>>>(L, genes, P, ngenes, out);
-        break;
-    case 64:
-        e = cudaFuncSetAttribute(pose_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) pose_kernel<64><<<(unsigned)blocks, 64, smem, st>>>(L, genes, P, ngenes, out);
-        break;
-    default:
-        e = cudaFuncSetAttribute(pose_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) pose_kernel<32><<<(unsigned)blocks, 32, smem, st>>>(L, genes, P, ngenes, out);
+#define VD_P(N)                                                                                   \
+    if (npp == N) {                                                                               \
+        e = cudaFuncSetAttribute(pose_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e == cudaSuccess) pose_kernel<N><<<(unsigned)blocks, N, smem, st>>>(L, genes, P, ngenes, lay, out); \
     }
+    VD_P(64) else VD_P(32) else VD_P(16) else return cudaErrorInvalidConfiguration;
+#undef VD_P
     if (e != cudaSuccess) return e;
     ++vdi::g_launches;
     return cudaGetLastError();
