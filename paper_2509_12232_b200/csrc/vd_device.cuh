@@ -176,18 +176,44 @@ __device__ __forceinline__ void torsion_axis(float2 ax, float2 ay, float2 az, fl
     kz = f2(k[0][2], k[1][2]);
 }
 
-/* Build poses g0 -> .x and g1 -> .y of the tile column S (S already offset by pp). */
+/* Scratch floats per pose pair (TPP > 1): rigid m/t of both poses (24) and the
+ * current torsion's axis k and cos/sin for both poses (10). */
+constexpr int kPoseScratch = 34;
+
+/* Build poses g0 -> .x and g1 -> .y of the tile column S (S already offset by pp).
+ * TPP > 1: the per-pose fp64 scalars (matrix, torsion axes, sincos) are computed
+ * once -- sub 0 for pose 0, sub 1 for pose 1 -- and shared through the scratch
+ * column X instead of being replicated by every sub. */
 template <int NPP, int TPP>
 __device__ __forceinline__ void build_pose2(const LigView &L, const double *__restrict__ g0,
-                                            const double *__restrict__ g1, float2 *S, int sub)
+                                            const double *__restrict__ g1, float2 *S, int sub,
+                                            float *X)
 {
-    float m0[9], t0[3], m1[9], t1[3];
-    rigid_of(g0, m0, t0);
-    rigid_of(g1, m1, t1);
-    const float2 M00 = f2(m0[0], m1[0]), M01 = f2(m0[1], m1[1]), M02 = f2(m0[2], m1[2]);
-    const float2 M10 = f2(m0[3], m1[3]), M11 = f2(m0[4], m1[4]), M12 = f2(m0[5], m1[5]);
-    const float2 M20 = f2(m0[6], m1[6]), M21 = f2(m0[7], m1[7]), M22 = f2(m0[8], m1[8]);
-    const float2 TX = f2(t0[0], t1[0]), TY = f2(t0[1], t1[1]), TZ = f2(t0[2], t1[2]);
+#define VD_X(k) X[(k) * NPP]
+    float2 M00, M01, M02, M10, M11, M12, M20, M21, M22, TX, TY, TZ;
+    if (TPP == 1) {
+        float m0[9], t0[3], m1[9], t1[3];
+        rigid_of(g0, m0, t0);
+        rigid_of(g1, m1, t1);
+        M00 = f2(m0[0], m1[0]); M01 = f2(m0[1], m1[1]); M02 = f2(m0[2], m1[2]);
+        M10 = f2(m0[3], m1[3]); M11 = f2(m0[4], m1[4]); M12 = f2(m0[5], m1[5]);
+        M20 = f2(m0[6], m1[6]); M21 = f2(m0[7], m1[7]); M22 = f2(m0[8], m1[8]);
+        TX = f2(t0[0], t1[0]); TY = f2(t0[1], t1[1]); TZ = f2(t0[2], t1[2]);
+    } else {
+        if (sub < 2) {
+            float m[9], t[3];
+            rigid_of(sub ? g1 : g0, m, t);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) VD_X(12 * sub + k) = m[k];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) VD_X(12 * sub + 9 + k) = t[k];
+        }
+        __syncthreads();
+        M00 = f2(VD_X(0), VD_X(12)); M01 = f2(VD_X(1), VD_X(13)); M02 = f2(VD_X(2), VD_X(14));
+        M10 = f2(VD_X(3), VD_X(15)); M11 = f2(VD_X(4), VD_X(16)); M12 = f2(VD_X(5), VD_X(17));
+        M20 = f2(VD_X(6), VD_X(18)); M21 = f2(VD_X(7), VD_X(19)); M22 = f2(VD_X(8), VD_X(20));
+        TX = f2(VD_X(9), VD_X(21)); TY = f2(VD_X(10), VD_X(22)); TZ = f2(VD_X(11), VD_X(23));
+    }
     for (int i = sub; i < L.n_atoms; i += TPP) {
         const float4 c = L.atom[i];
         const float2 cx = f2(c.x), cy = f2(c.y), cz = f2(c.z);
@@ -199,14 +225,37 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
     for (int t = 0; t < L.n_torsions; ++t) {
         const int4 tr = L.tors[t];
         const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
-        float2 KX, KY, KZ;
-        torsion_axis(sub2(VD_S2(tr.y, 0), ox), sub2(VD_S2(tr.y, 1), oy), sub2(VD_S2(tr.y, 2), oz),
-                     KX, KY, KZ);
-        double s0, c0, s1, c1;
-        sincos(g0[7 + t], &s0, &c0);
-        sincos(g1[7 + t], &s1, &c1);
-        const float2 C = f2(__double2float_rn(c0), __double2float_rn(c1));
-        const float2 SN = f2(__double2float_rn(s0), __double2float_rn(s1));
+        float2 KX, KY, KZ, C, SN;
+        if (TPP == 1) {
+            torsion_axis(sub2(VD_S2(tr.y, 0), ox), sub2(VD_S2(tr.y, 1), oy),
+                         sub2(VD_S2(tr.y, 2), oz), KX, KY, KZ);
+            double s0, c0, s1, c1;
+            sincos(g0[7 + t], &s0, &c0);
+            sincos(g1[7 + t], &s1, &c1);
+            C = f2(__double2float_rn(c0), __double2float_rn(c1));
+            SN = f2(__double2float_rn(s0), __double2float_rn(s1));
+        } else {
+            if (sub < 2) {
+                const float ax = __fsub_rn(sub ? VD_S2(tr.y, 0).y : VD_S2(tr.y, 0).x, sub ? ox.y : ox.x);
+                const float ay = __fsub_rn(sub ? VD_S2(tr.y, 1).y : VD_S2(tr.y, 1).x, sub ? oy.y : oy.x);
+                const float az = __fsub_rn(sub ? VD_S2(tr.y, 2).y : VD_S2(tr.y, 2).x, sub ? oz.y : oz.x);
+                const double x = (double)ax, y = (double)ay, z = (double)az;
+                const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+                double sd, cd;
+                sincos((sub ? g1 : g0)[7 + t], &sd, &cd);
+                VD_X(24 + 5 * sub + 0) = __double2float_rn(__ddiv_rn(x, n));
+                VD_X(24 + 5 * sub + 1) = __double2float_rn(__ddiv_rn(y, n));
+                VD_X(24 + 5 * sub + 2) = __double2float_rn(__ddiv_rn(z, n));
+                VD_X(24 + 5 * sub + 3) = __double2float_rn(cd);
+                VD_X(24 + 5 * sub + 4) = __double2float_rn(sd);
+            }
+            __syncthreads();
+            KX = f2(VD_X(24), VD_X(29));
+            KY = f2(VD_X(25), VD_X(30));
+            KZ = f2(VD_X(26), VD_X(31));
+            C = f2(VD_X(27), VD_X(32));
+            SN = f2(VD_X(28), VD_X(33));
+        }
         const float2 OMC = sub2(f2(1.0f), C);
 #pragma unroll 4
         for (int f = tr.z + sub; f < tr.w; f += TPP) {
@@ -224,6 +273,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
         }
         if (TPP > 1) __syncthreads();
     }
+#undef VD_X
 }
 
 /* ---- A2: inter ------------------------------------------------------------ */
@@ -607,7 +657,7 @@ __device__ __forceinline__ void reduce_subs(double *red, int pp, int sub, double
 
 /* Dynamic shared-memory layout of the scoring CTAs. */
 struct SmemLayout {
-    unsigned topo_atom, topo_atom2, topo_tors, topo_frag;
+    unsigned topo_atom, topo_atom2, topo_tors, topo_frag, scratch;
     unsigned tile_coef, tile_j, tile_row, red, extra, bytes;
 };
 
@@ -626,14 +676,22 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     off = align16(off + 16u * (unsigned)n_tors);
     s.topo_frag = off;
     off = align16(off + 4u * (unsigned)n_frag);
+    s.scratch = off;
+    off = align16(off + ((tpp > 1) ? 4u * kPoseScratch * (unsigned)npp : 0u));
     s.tile_coef = off;
     off += 16u * kTile;
     s.tile_row = off;
     off += 16u * kTile;
     s.tile_j = off;
     off += 4u * kTile;
-    s.red = off;
-    off += (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
+    /* sub reduction reuses the pair tiles (intra is finished when it runs) */
+    const unsigned red_bytes = (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
+    if (red_bytes <= 36u * kTile) {
+        s.red = s.tile_coef;
+    } else {
+        s.red = off;
+        off += red_bytes;
+    }
     s.extra = align16(off);
     s.bytes = align16(s.extra + extra);
     return s;

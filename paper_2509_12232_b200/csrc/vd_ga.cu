@@ -187,7 +187,8 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
             for (int b0 = 0; b0 < pop; b0 += 2 * NPP) {
                 const int i0 = b0 + 2 * pp, i1 = i0 + 1;
                 const int q0 = min(i0, pop - 1), q1 = min(i1, pop - 1);
-                build_pose2<NPP, TPP>(L, cur + (size_t)q0 * G, cur + (size_t)q1 * G, S, sub);
+                build_pose2<NPP, TPP>(L, cur + (size_t)q0 * G, cur + (size_t)q1 * G, S, sub,
+                                      reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 inter2<EXACT, NPP, TPP>(L, Gv, S, sub, e0, e1);
                 intra2<EXACT, NPP, TPP>(L, S, Tl, sub, a0, a1);

@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
     const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;  /* tail: duplicate, drop */
     if (genes) {
-        build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub);
+        build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
+                              reinterpret_cast<float *>(smem + lay.scratch) + pp);
     } else {
         const int n = L.n_atoms;
         const float *s0 = poses + q0 * 3 * n, *s1 = poses + q1 * 3 * n;
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
     const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;
-    build_pose2<NPP, 1>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, 0);
+    build_pose2<NPP, 1>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, 0, nullptr);
     const int n = L.n_atoms;
     for (int i = 0; i < n; ++i)
 #pragma unroll
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
 int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
 {
     const unsigned limit = 200 * 1024;
-    int t = exact ? 1 : (n_atoms <= 40 ? 1 : (n_atoms <= 80 ? 2 : 4));
+    int t = exact ? 1 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 2 : 4));
     if (!exact)
         if (const char *ov = getenv("VD_TPP")) {  /* tuning override: 1, 2 or 4 */
             const int v = atoi(ov);
