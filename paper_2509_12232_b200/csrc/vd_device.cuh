@@ -191,6 +191,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
 {
 #define VD_X(k) X[(k) * NPP]
     float2 M00, M01, M02, M10, M11, M12, M20, M21, M22, TX, TY, TZ;
+    if (TPP > 1) __syncthreads();  /* scratch aliases tiles still read by the previous pose */
     if (TPP == 1) {
         float m0[9], t0[3], m1[9], t1[3];
         rigid_of(g0, m0, t0);
@@ -664,7 +665,7 @@ struct SmemLayout {
 __host__ __device__ inline unsigned align16(unsigned v) { return (v + 15u) & ~15u; }
 
 __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n_frag, int npp,
-                                                  int tpp, unsigned extra)
+                                                  int tpp, unsigned extra, bool alias = true)
 {
     SmemLayout s;
     unsigned off = align16(8u * 3u * (unsigned)n_atoms * (unsigned)npp);
@@ -676,8 +677,15 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     off = align16(off + 16u * (unsigned)n_tors);
     s.topo_frag = off;
     off = align16(off + 4u * (unsigned)n_frag);
-    s.scratch = off;
-    off = align16(off + ((tpp > 1) ? 4u * kPoseScratch * (unsigned)npp : 0u));
+    /* pose-build scratch aliases the pair tiles (the pose is built before intra
+       stages pairs; build_pose2 syncs before its first scratch write) */
+    const unsigned scratch_bytes = (tpp > 1) ? 4u * kPoseScratch * (unsigned)npp : 0u;
+    if (!alias || scratch_bytes > 36u * kTile) {
+        s.scratch = off;
+        off = align16(off + scratch_bytes);
+    } else {
+        s.scratch = off;  /* == tile_coef below */
+    }
     s.tile_coef = off;
     off += 16u * kTile;
     s.tile_row = off;

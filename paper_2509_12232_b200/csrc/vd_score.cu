@@ -96,7 +96,11 @@ int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
             const int v = atoi(ov);
             if (v == 1 || v == 2 || v == 4) t = v;
         }
+    int force_npp = 0;
+    if (!exact)
+        if (const char *ov = getenv("VD_NPP")) force_npp = atoi(ov);  /* tuning override */
     for (int n : {64, 32, 16}) {
+        if (force_npp && n != force_npp) continue;
         if (smem_layout(n_atoms, 64, 4 * n_atoms, n, t, 0).bytes <= limit) {
             *npp = n;
             *tpp = t;
@@ -113,7 +117,10 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
                             const float *poses, int64_t P, int ngenes, double *inter,
                             double *intra, float *total, cudaStream_t st)
 {
-    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0);
+    /* aliasing the pose scratch into the pair tiles buys a third CTA per SM at
+       TPP=2 but measured 24% slower on B200 (2.98 vs 2.40 ms, cfg1); opt-in only */
+    static const bool alias = getenv("VD_ALIAS") != nullptr;
+    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0, alias);
     auto k = score_kernel<EXACT, NPP, TPP>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
     if (e != cudaSuccess) return e;
