@@ -665,7 +665,7 @@ struct SmemLayout {
 __host__ __device__ inline unsigned align16(unsigned v) { return (v + 15u) & ~15u; }
 
 __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n_frag, int npp,
-                                                  int tpp, unsigned extra, bool alias = true)
+                                                  int tpp, unsigned extra, bool alias = false)
 {
     SmemLayout s;
     unsigned off = align16(8u * 3u * (unsigned)n_atoms * (unsigned)npp);
