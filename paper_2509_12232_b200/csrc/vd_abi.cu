@@ -192,6 +192,12 @@ int vd_init(int device)
 {
     VD_CK(cudaSetDevice(device));
     VD_CK(cudaFree(0));
+    /* keep stream-ordered staging buffers in the pool between calls instead of
+       returning them to the OS at every synchronisation */
+    cudaMemPool_t pool;
+    VD_CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    VD_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
     return 0;
 }
 
