@@ -40,6 +40,10 @@ UNIT = "poses/s"
 N_POSES = 1_000_000
 WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
+# dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
+# committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
+TRAFFIC_BYTES = 158.22e6 + 19.94e6
+TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch)"
 
 
 def env_int(k, d):
@@ -257,8 +261,9 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(N_POSES * (8 + 8 + 4)),
                 "path": "CudaBackend.score_population_arrays (pinned numpy in/out)"},
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": FP32_SPEC_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP32_SPEC_TFLOPS, "traffic": None,
-                     "kernel": "vd::score_kernel<false,128,0>",
+                     "unit": "TFLOP/s", "frac": achieved / FP32_SPEC_TFLOPS,
+                     "traffic": TRAFFIC_BYTES, "traffic_source": TRAFFIC_SRC,
+                     "kernel": "vd::score_kernel<false,64,2>",
                      "algorithmic_flops_per_pose": fpp,
                      "peak_source": "spec-derived 2*128 lanes*148 SMs*1.965 GHz (no measured "
                                     "FP32 figure in MEASURED_PEAKS.json)"},
