@@ -286,11 +286,10 @@ def screening_leg(args, rank, world, dist, dev):
     generations), ligands split by index over ranks, records all-gathered over NCCL."""
     import torch
 
-    from paper_2509_12232_b200 import context, gridmaps, synth
+    from paper_2509_12232_b200 import gridmaps, hostprep, synth
     from paper_2509_12232_b200.backend import CudaBackend
     from paper_2509_12232_b200.ga import GaConfig, _run
-    from paper_2509_12232_b200.screening import (_shared_device_set, gather_records,
-                                                 pack_records, shard_range)
+    from paper_2509_12232_b200.screening import gather_records, pack_records, shard_range
 
     cfg = synth.CONFIGS[2]
     spec = synth.config_grid_spec(2)
@@ -298,22 +297,24 @@ def screening_leg(args, rank, world, dist, dev):
     n = args.screen_ligands
     lo, hi = shard_range(n, rank, world)
     t0 = time.perf_counter()
-    ligs = [synth.config_ligand(2, i) for i in range(lo, hi)]
-    ctxs = [context.prepare_context(l, gset) for l in ligs]
+    batch = hostprep.TopologyBatch.synth(2, lo, hi - lo)       # this rank's ligand range only
+    arrays = hostprep.prepare_batch(batch, list(gset.maps))
     prep_s = time.perf_counter() - t0
     b = CudaBackend(mode="fast", device=dev.index)
-    grid, lset = _shared_device_set(b, gset, ctxs)
-    gmax = 7 + max(c.n_torsions for c in ctxs)
+    grid = b._grid_for_set(gset)
+    lset = hostprep.ligand_set(arrays)
+    gmax = 7 + int(batch.n_torsions.max())
     ga = GaConfig(population_size=256, generations=200,
                   translation_bounds=(spec.origin, spec.upper))
-    _run(grid, lset, 0, min(8, len(ctxs)), GaConfig(population_size=256, generations=2,
+    count = hi - lo
+    _run(grid, lset, 0, min(8, count), GaConfig(population_size=256, generations=2,
          translation_bounds=(spec.origin, spec.upper)), 0, lo, b._mode(), gmax, trace=False)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    bt, be, ba, bg, _, ne = _run(grid, lset, 0, len(ctxs), ga, 0, lo, b._mode(), gmax,
+    bt, be, ba, bg, _, ne = _run(grid, lset, 0, count, ga, 0, lo, b._mode(), gmax,
                                  trace=False)
     ev1.record()
     torch.cuda.synchronize(dev)
@@ -330,8 +331,9 @@ def screening_leg(args, rank, world, dist, dev):
     return {"metric": "ligands docked/sec", "value": n / t_max, "unit": "ligands/s",
             "pose_evals_per_s": evals / t_max, "ligands": n, "ms": 1e3 * t_max,
             "ga": "pop 256 x 200 generations (cfg2 distribution, 64^3 grid, 3000-atom receptor)",
+            "workload": "cfg2-screen-10k" if n == 10000 else f"cfg2-distribution x{n}",
             "gathered_records": int(rec.shape[0]), "gather_ms": round(1e3 * t_gather, 3),
-            "host_prep_s_per_rank": round(prep_s, 2),
+            "host_prep_s_per_rank": round(prep_s, 3),
             "timing": "CUDA events around the one persistent GA launch, max over ranks"}
 
 
@@ -403,7 +405,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=16384)
-    ap.add_argument("--screen-ligands", type=int, default=1024,
+    ap.add_argument("--screen-ligands", type=int, default=10000,
                     help="cfg2 ligands for the ligands/s leg (0 disables)")
     args = ap.parse_args()
     if args.warmup < 3:

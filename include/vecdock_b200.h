@@ -132,6 +132,32 @@ int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, int count,
                   float *trace /* nullable [count][generations + 1] */, int64_t *n_evals,
                   void *stream);
 
+/* ---- batched host preprocessing (no device needed) ----------------------- */
+/* Restates build_nonbond_pairlist / build_fragment_masks / prepare_context
+ * (vd/model.py:174-269, vd/scoring/__init__.py:117-207) bit for bit for many
+ * ligands (OpenMP).  Pass 1 sizes the CSR; pass 2 fills vd_ligand_arrays fields.
+ * xyz is (3, n) per ligand at 3*atom_start[l]; bonds/axes are index pairs. */
+int vd_prepare_count(int n_ligands, const int32_t *atom_start, const float *xyz,
+                     const int32_t *bond_start, const int32_t *bonds, const int32_t *tors_start,
+                     const int32_t *axes, int64_t *n_pairs, int64_t *n_frag);
+int vd_prepare_fill(int n_ligands, const int32_t *atom_start, const float *xyz,
+                    const int32_t *type_index, const float *charge, const int32_t *bond_start,
+                    const int32_t *bonds, const int32_t *tors_start, const int32_t *axes,
+                    const vd_atom_type *table, int n_types, const int32_t *type_map,
+                    const vd_weights *w, double w_tors, const int64_t *pair_start,
+                    const int64_t *frag_start, float *centered0, float *dsf, int32_t *atom_map,
+                    int32_t *pair_i, int32_t *pair_j, float *pair_a, float *pair_b,
+                    float *pair_qq, float *pair_dsl, uint8_t *pair_hb, int32_t *frag_lo,
+                    int32_t *frag_hi, int32_t *frag_index, float *torsional32);
+
+/* Synthetic cfg2/3/4 ligands, counter-keyed per index. */
+int vd_synth_count(uint64_t seed, int64_t first, int count, int h_lo, int h_hi, double hd_ratio,
+                   int t_lo, int t_hi, int32_t *n_atoms, int32_t *n_tors_max);
+int vd_synth_fill(uint64_t seed, int64_t first, int count, int h_lo, int h_hi, double hd_ratio,
+                  int t_lo, int t_hi, const int32_t *heavy_types, int32_t hd_type,
+                  const int32_t *atom_start, float *xyz, int32_t *type_index, float *charge,
+                  int32_t *bonds, int32_t *n_tors, int32_t *axes);
+
 /* device-side counters of the last call on this thread (kernel launches) */
 int vd_last_launch_count(int64_t *launches);
 

@@ -63,6 +63,7 @@ EXPORTS = (
     "vd_grid_build", "vd_grid_n_maps", "vd_grid_download", "vd_grid_destroy",
     "vd_ligands_create", "vd_ligands_n_torsions", "vd_ligands_destroy", "vd_score_genes",
     "vd_score_poses", "vd_pose_genes", "vd_dock_batch", "vd_last_launch_count",
+    "vd_prepare_count", "vd_prepare_fill", "vd_synth_count", "vd_synth_fill",
 )
 
 
@@ -92,7 +93,22 @@ def load_library(path: Path = LIB_PATH):
     L.vd_dock_batch.argtypes = [vp, vp, i32, i32, vp, u64, i64, i32, vp, vp, vp, vp, i32, vp,
                                 vp, vp]
     L.vd_last_launch_count.argtypes = [vp]
+    L.vd_prepare_count.argtypes = [i32] + [vp] * 8
+    L.vd_prepare_fill.argtypes = [i32] + [vp] * 8 + [vp, i32, vp, vp, C.c_double] + [vp] * 16
+    L.vd_synth_count.argtypes = [u64, i64, i32, i32, i32, C.c_double, i32, i32, vp, vp]
+    L.vd_synth_fill.argtypes = [u64, i64, i32, i32, i32, C.c_double, i32, i32, vp, i32] + [vp] * 7
     return L
+
+
+_host_lib = None
+
+
+def host_lib():
+    """The library for host-only entry points (no device required)."""
+    global _host_lib
+    if _host_lib is None:
+        _host_lib = _lib if _lib is not None else load_library()
+    return _host_lib
 
 
 def lib():
@@ -236,6 +252,24 @@ def build_grid(protein, spec, probe_types, weights, table, cutoff, device=None) 
 # --- ligand sets -------------------------------------------------------------------
 class LigandSet:
     """Owned vd_ligands handle over a list of scoring contexts (CSR)."""
+
+    @classmethod
+    def from_arrays(cls, keep: dict, elec_map: int, desolv_map: int):
+        """Build directly from vd_ligand_arrays-shaped numpy arrays (hostprep batches)."""
+        ensure_device()
+        self = cls.__new__(cls)
+        a = VdLigandArrays()
+        a.n_ligands = len(keep["atom_start"]) - 1
+        for k, v in keep.items():
+            setattr(a, k, v.ctypes.data if v.size else None)
+        a.elec_map, a.desolv_map = int(elec_map), int(desolv_map)
+        h = C.c_void_p()
+        check(lib().vd_ligands_create(C.byref(a), C.byref(h)), "vd_ligands_create")
+        self.handle = h
+        self.n_ligands = a.n_ligands
+        self.n_atoms = np.diff(keep["atom_start"])
+        self.n_torsions = np.diff(keep["tors_start"])
+        return self
 
     def __init__(self, contexts, atom_maps, elec_map: int, desolv_map: int):
         ensure_device()

@@ -276,6 +276,35 @@ cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const Li
     return cudaErrorInvalidConfiguration;
 }
 
+template <bool EXACT, int NPP, int TPP>
+static int occ_t(unsigned bytes)
+{
+    auto k = ga_kernel<EXACT, NPP, TPP>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NPP * TPP, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per_sm;
+}
+
+/* resident CTAs per SM for a GA shape (registers and shared memory both count) */
+int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes)
+{
+#define VD_O(EX, N, T) \
+    if (exact == EX && npp == N && tpp == T) return occ_t<EX, N, T>(bytes)
+    VD_O(true, 64, 1); VD_O(true, 32, 1); VD_O(true, 16, 1);
+    VD_O(false, 64, 1); VD_O(false, 32, 1); VD_O(false, 16, 1);
+    VD_O(false, 64, 2); VD_O(false, 32, 2); VD_O(false, 16, 2);
+    VD_O(false, 64, 4); VD_O(false, 32, 4); VD_O(false, 16, 4);
+#undef VD_O
+    return 0;
+}
+
 }  // namespace vd
 
 using vdi::set_error;
@@ -297,49 +326,79 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         return -1;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    /* ligand views + largest-first order */
+    const bool exact = mode == VD_MODE_EXACT;
+    /* ligand views, bucketed by atom count (each bucket gets its own pose-tile
+       size and launch shape), largest-first inside a bucket */
+    static const int kBucketEdge[] = {24, 32, 48, 64, 96, 128, 192, 256, 1 << 30};
+    constexpr int kBuckets = sizeof(kBucketEdge) / sizeof(int);
     std::vector<vd::LigView> views(count);
-    std::vector<int> order(count);
-    int nmax = 1, tmax = 0, fmax = 0;
+    std::vector<std::vector<int>> bucket(kBuckets);
+    int tmax = 0;
     for (int l = 0; l < count; ++l) {
         views[l] = s->view(first + l);
-        nmax = std::max(nmax, views[l].n_atoms);
         tmax = std::max(tmax, views[l].n_torsions);
-        fmax = std::max(fmax, views[l].n_frag);
-        order[l] = l;
+        int b = 0;
+        while (views[l].n_atoms > kBucketEdge[b]) ++b;
+        bucket[b].push_back(l);
     }
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-        const int64_t ca = (int64_t)views[a].n_pairs + 4 * views[a].n_atoms;
-        const int64_t cb = (int64_t)views[b].n_pairs + 4 * views[b].n_atoms;
-        return ca > cb;
-    });
     const int gmax = 7 + tmax;
     if (gstride < gmax) {
         set_error("vd_dock_batch: gstride smaller than 7 + max torsions");
         return -1;
     }
-    const bool exact = mode == VD_MODE_EXACT;
-    int npp, tpp;
-    if (vd::pick_shape(nmax, exact, &npp, &tpp)) return -1;
-    vd::GaLayout lay;
+    std::vector<int> order;
+    struct Launch {
+        int off, cnt, npp, tpp;
+        vd::GaLayout lay;
+    };
+    std::vector<Launch> launches;
     const unsigned extra = (unsigned)p->pop * (4u + 8u + 8u + 1u) + 64u;
-    for (;;) {
-        lay.base = vd::smem_layout(nmax, tmax, fmax, npp, tpp, extra);
-        if (lay.base.bytes <= 227u * 1024u || npp == 16) break;
-        npp /= 2;
+    for (int b = 0; b < kBuckets; ++b) {
+        if (bucket[b].empty()) continue;
+        auto &v = bucket[b];
+        std::stable_sort(v.begin(), v.end(), [&](int x, int y) {
+            return (int64_t)views[x].n_pairs + 4 * views[x].n_atoms >
+                   (int64_t)views[y].n_pairs + 4 * views[y].n_atoms;
+        });
+        int nmax = 1, tb = 0, fb = 0;
+        for (int l : v) {
+            nmax = std::max(nmax, views[l].n_atoms);
+            tb = std::max(tb, views[l].n_torsions);
+            fb = std::max(fb, views[l].n_frag);
+        }
+        Launch L;
+        int npp0;
+        if (vd::pick_shape(nmax, exact, &npp0, &L.tpp)) return -1;
+        /* pose-pairs per CTA: the candidate with most resident warps per SM */
+        int best_warps = -1;
+        for (int npp : {64, 32, 16}) {
+            vd::GaLayout lay;
+            lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra);
+            if (lay.base.bytes > 227u * 1024u) continue;
+            const int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes) * npp * L.tpp / 32;
+            if (warps > best_warps) {
+                best_warps = warps;
+                L.npp = npp;
+                L.lay = lay;
+            }
+        }
+        if (best_warps <= 0) {
+            set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
+            return -1;
+        }
+        unsigned off = L.lay.base.extra;
+        L.lay.off_e = off;
+        off += 8u * p->pop;
+        L.lay.off_a = off;
+        off += 8u * p->pop;
+        L.lay.off_fit = off;
+        off += 4u * p->pop;
+        L.lay.off_taken = off;
+        L.off = (int)order.size();
+        L.cnt = (int)v.size();
+        order.insert(order.end(), v.begin(), v.end());
+        launches.push_back(L);
     }
-    if (lay.base.bytes > 227u * 1024u) {
-        set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
-        return -1;
-    }
-    unsigned off = lay.base.extra;
-    lay.off_e = off;
-    off += 8u * p->pop;
-    lay.off_a = off;
-    off += 8u * p->pop;
-    lay.off_fit = off;
-    off += 4u * p->pop;
-    lay.off_taken = off;
     vd::GaDev P;
     P.pop = p->pop; P.generations = p->generations; P.tournament = p->tournament;
     P.elitism = p->elitism;
@@ -357,10 +416,10 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     const size_t G1 = (size_t)p->generations + 1;
     VD_CK(cudaMallocAsync((void **)&d_views, sizeof(vd::LigView) * count, st));
     VD_CK(cudaMallocAsync((void **)&d_order, sizeof(int) * count, st));
-    VD_CK(cudaMallocAsync((void **)&d_work, sizeof(int), st));
+    VD_CK(cudaMallocAsync((void **)&d_work, sizeof(int) * launches.size(), st));
     VD_CK(cudaMemcpyAsync(d_views, views.data(), sizeof(vd::LigView) * count, cudaMemcpyHostToDevice, st));
     VD_CK(cudaMemcpyAsync(d_order, order.data(), sizeof(int) * count, cudaMemcpyHostToDevice, st));
-    VD_CK(cudaMemsetAsync(d_work, 0, sizeof(int), st));
+    VD_CK(cudaMemsetAsync(d_work, 0, sizeof(int) * launches.size(), st));
     if (!dev_out) {
         VD_CK(cudaMallocAsync((void **)&d_bt, sizeof(float) * count, st));
         VD_CK(cudaMallocAsync((void **)&d_be, sizeof(double) * count, st));
@@ -373,9 +432,15 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     vd::GaOut o;
     o.best_total = d_bt; o.best_inter = d_be; o.best_intra = d_ba; o.best_genes = d_bg;
     o.gstride = gstride; o.trace = d_tr; o.n_evals = d_ne;
-    int n_ctas = 0;
-    VD_CK(vd::launch_ga(exact, npp, tpp, vdi::grid_view(g, s->elec_map, s->desolv_map), d_views, d_order, count, P, seed,
-                        lig_index_base, gmax, lay, o, st, d_work, &gene_buf, &n_ctas));
+    const vd::GridView gv = vdi::grid_view(g, s->elec_map, s->desolv_map);
+    for (size_t b = 0; b < launches.size(); ++b) {
+        const Launch &L = launches[b];
+        int n_ctas = 0;
+        gene_buf = nullptr;
+        VD_CK(vd::launch_ga(exact, L.npp, L.tpp, gv, d_views, d_order + L.off, L.cnt, P, seed,
+                            lig_index_base, gmax, L.lay, o, st, d_work + b, &gene_buf, &n_ctas));
+        cudaFreeAsync(gene_buf, st);
+    }
     if (!dev_out) {
         VD_CK(cudaMemcpyAsync(best_total, d_bt, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
         VD_CK(cudaMemcpyAsync(best_inter, d_be, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
@@ -387,7 +452,6 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         cudaFreeAsync(d_bg, st); cudaFreeAsync(d_ne, st);
         if (trace) cudaFreeAsync(d_tr, st);
     }
-    cudaFreeAsync(gene_buf, st);
     cudaFreeAsync(d_views, st);
     cudaFreeAsync(d_order, st);
     cudaFreeAsync(d_work, st);

@@ -99,8 +99,7 @@ def gather_records(rec: np.ndarray, n_total: int, dist=None, device=None) -> np.
     return out.cpu().numpy()[:n_total]
 
 
-def screen_batch(batch, grid_set, config: ScreenConfig, weights=None, table=None,
-                 chunk: int = 8192) -> list:
+def screen_batch(batch, grid_set, config: ScreenConfig, weights=None, table=None) -> list:
     """Dock every ligand; one ScreenEntry per ligand in input order (vd/screening.py:165-244)."""
     from .backend import get_backend
 
@@ -118,18 +117,33 @@ def screen_batch(batch, grid_set, config: ScreenConfig, weights=None, table=None
     lo, hi = shard_range(n, rank, world)
     gmax = 7 + max(t.n_torsions for _, t in entries)
 
-    # host prep for this shard; one context per unique topology object
-    ctx_of, errors = {}, {}
-    for idx in range(lo, hi):
-        topo = entries[idx][1]
-        if id(topo) in ctx_of or id(topo) in errors:
-            continue
-        try:
-            ctx_of[id(topo)] = prepare_context(topo, grid_set, weights=weights, table=table)
-        except Exception as exc:  # recorded in place, batch continues (vd/screening.py:195-203)
-            errors[id(topo)] = f"{type(exc).__name__}: {exc}"
+    # host prep for this shard: the C++ batch path (csrc/vd_host.cpp, bit-identical to
+    # prepare_context); if any ligand fails it, fall back per ligand so failures are
+    # recorded in place and the batch continues (vd/screening.py:195-203)
+    from . import hostprep
 
+    errors = {}
+    good = list(range(lo, hi))
     t0 = time.perf_counter()
+    grid = b._grid_for_set(grid_set)
+    ligs = None
+    try:
+        batch = hostprep.TopologyBatch.from_topologies([entries[i][1] for i in good])
+        ligs = hostprep.ligand_set(
+            hostprep.prepare_batch(batch, grid.labels, weights=weights, table=table))
+    except Exception:
+        # per-ligand Python contexts (stored fragments, exact reference semantics)
+        ctxs, ok_idx = [], []
+        for idx in good:
+            try:
+                ctxs.append(prepare_context(entries[idx][1], grid_set, weights=weights,
+                                            table=table))
+                ok_idx.append(idx)
+            except Exception as exc:
+                errors[idx] = f"{type(exc).__name__}: {exc}"
+        good = ok_idx
+        if good:
+            _, ligs = _shared_device_set(b, grid_set, ctxs)
     m = hi - lo
     bt = np.full(m, np.nan, np.float32)
     be = np.full(m, np.nan)
@@ -137,18 +151,12 @@ def screen_batch(batch, grid_set, config: ScreenConfig, weights=None, table=None
     ne = np.zeros(m, np.int64)
     bg = np.zeros((m, gmax))
     ok = np.zeros(m)
-    good = [i for i in range(lo, hi) if id(entries[i][1]) in ctx_of]
-    for c0 in range(0, len(good), chunk):
-        part = good[c0:c0 + chunk]
-        ctxs = [ctx_of[id(entries[i][1])] for i in part]
-        grid, ligs = _shared_device_set(b, grid_set, ctxs)
-        # ligand index i keys its stream (global_seed, i): pass each as its own base
-        # by running contiguous runs of indices as one launch
-        for run_lo, run_hi in _runs(part):
-            k0 = part.index(run_lo)
-            cnt = run_hi - run_lo
-            r = _run(grid, ligs, k0, cnt, ga, config.global_seed, run_lo, b._mode(), gmax,
-                     trace=False)
+    if good:
+        # ligand index i keys its stream (global_seed, i): consecutive index runs share a launch
+        for run_lo, run_hi in _runs(good):
+            k0 = good.index(run_lo)
+            r = _run(grid, ligs, k0, run_hi - run_lo, ga, config.global_seed, run_lo, b._mode(),
+                     gmax, trace=False)
             s = slice(run_lo - lo, run_hi - lo)
             bt[s], be[s], ba[s], bg[s], ne[s] = r[0], r[1], r[2], r[3], r[5]
             ok[s] = 1
@@ -161,7 +169,7 @@ def screen_batch(batch, grid_set, config: ScreenConfig, weights=None, table=None
         r = allrec[idx]
         key = (config.global_seed, idx)
         if r[4] != 1:
-            err = errors.get(id(topo)) or "ligand failed on its rank"
+            err = errors.get(idx) or "ligand failed on its rank"
             out.append(ScreenEntry(name, None, err, float("nan"), key))
             continue
         G = 7 + topo.n_torsions
