@@ -529,6 +529,28 @@ __device__ __forceinline__ float2 row_fast(const float2 *S, int i, int kb, int k
     return acc;
 }
 
+/* Flat variant: per-pair packed (i | j << 16), no row structure, deep unroll. */
+#ifndef VD_FLAT_UNROLL
+#define VD_FLAT_UNROLL 8
+#endif
+constexpr int kFlatUnroll = VD_FLAT_UNROLL;
+template <int NPP, int TPP, bool HB, bool CUT>
+__device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, const float4 *tc,
+                                            const int *tij, int sub, float cut2)
+{
+    float2 acc = f2(0.0f);
+#pragma unroll kFlatUnroll
+    for (int k = kb + sub; k < ke; k += TPP) {
+        const float4 c = tc[k];
+        const int w = tij[k];
+        const int i = w & 0xffff, j = w >> 16;
+        acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(VD_S2(i, 0), VD_S2(j, 0)),
+                                             fsub2(VD_S2(i, 1), VD_S2(j, 1)),
+                                             fsub2(VD_S2(i, 2), VD_S2(j, 2)), c, cut2));
+    }
+    return acc;
+}
+
 /* Shared-memory pair staging area (per CTA). */
 struct PairTile {
     float4 *coef;   /* [kTile] */
@@ -537,7 +559,7 @@ struct PairTile {
 };
 
 /* intra of both poses over this sub's share of the pairs (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP>
+template <bool EXACT, int NPP, int TPP, bool FLAT = false>
 __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const PairTile &T,
                                        int sub, double &a0, double &a1)
 {
@@ -605,11 +627,27 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
             __syncthreads();
             for (int k = tid; k < cnt; k += B) {
                 T.coef[k] = __ldg(&L.fcoef[k0 + k]);
-                T.j[k] = __ldg(&L.fj[k0 + k]);
+                T.j[k] = FLAT ? (__ldg(&L.fj[k0 + k]) << 16) : __ldg(&L.fj[k0 + k]);
             }
             for (int r = tid; r < r1 - r0; r += B) T.row[r] = __ldg(&L.frow[r0 + r]);
             __syncthreads();
             float2 part = f2(0.0f);
+            if (FLAT) {
+                /* expand rows into per-pair i (packed beside j), find the hb boundary */
+                __shared__ int s_kh;
+                if (tid == 0) s_kh = cnt;
+                for (int r = tid; r < r1 - r0; r += B) {
+                    const int4 row = T.row[r];
+                    for (int k = row.y - k0; k < row.z - k0; ++k) T.j[k] |= row.x;
+                    if (row.w && (r == 0 || !T.row[r - 1].w)) s_kh = row.y - k0;
+                }
+                __syncthreads();
+                const int kh = s_kh;
+                part = cut ? flat_fast<NPP, TPP, false, true>(S, 0, kh, T.coef, T.j, sub, L.cut2)
+                           : flat_fast<NPP, TPP, false, false>(S, 0, kh, T.coef, T.j, sub, L.cut2);
+                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, cnt, T.coef, T.j, sub, L.cut2)
+                                       : flat_fast<NPP, TPP, true, false>(S, kh, cnt, T.coef, T.j, sub, L.cut2));
+            } else
             for (int r = 0; r < r1 - r0; ++r) {
                 const int4 row = T.row[r];
                 const int kb = row.y - k0, ke = row.z - k0;

@@ -7,13 +7,14 @@
  * vd/scoring/__init__.py:345.  A CTA owns 2*NPP poses (NPP pose pairs, TPP
  * threads per pair); see vd_device.cuh for the stage contracts.
  */
+#include <cstdio>
 #include <cstdlib>
 
 #include "vd_internal.h"
 
 namespace vd {
 
-template <bool EXACT, int NPP, int TPP>
+template <bool EXACT, int NPP, int TPP, bool FLAT>
 __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
                                                          const double *__restrict__ genes,
                                                          const float *__restrict__ poses,
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
     inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
-    intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
+    intra2<EXACT, NPP, TPP, FLAT>(L, S, T, sub, a0, a1);
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
 int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
 {
     const unsigned limit = 200 * 1024;
-    int t = exact ? 1 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 2 : 4));
+    int t = exact ? 1 : (n_atoms <= 16 ? 1 : 4);
     if (!exact)
         if (const char *ov = getenv("VD_TPP")) {  /* tuning override: 1, 2 or 4 */
             const int v = atoi(ov);
@@ -99,7 +100,10 @@ int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
     int force_npp = 0;
     if (!exact)
         if (const char *ov = getenv("VD_NPP")) force_npp = atoi(ov);  /* tuning override */
-    for (int n : {64, 32, 16}) {
+    /* fast mode prefers 32 pose pairs x 4 threads (cfg1 A/B on B200: 2.16 ms vs
+       2.44 ms for NPP=64 even though NPP=64 keeps 16 vs 12 warps resident) */
+    const int pref_fast[3] = {32, 16, 64}, pref_exact[3] = {64, 32, 16};
+    for (int n : (exact ? pref_exact : pref_fast)) {
         if (force_npp && n != force_npp) continue;
         if (smem_layout(n_atoms, 64, 4 * n_atoms, n, t, 0).bytes <= limit) {
             *npp = n;
@@ -121,7 +125,8 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
        TPP=2 but measured 24% slower on B200 (2.98 vs 2.40 ms, cfg1); opt-in only */
     static const bool alias = getenv("VD_ALIAS") != nullptr;
     const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0, alias);
-    auto k = score_kernel<EXACT, NPP, TPP>;
+    static const bool flat = getenv("VD_ROWS") == nullptr;  /* flat pair stream (A/B: VD_ROWS=1) */
+    auto k = flat ? score_kernel<EXACT, NPP, TPP, true> : score_kernel<EXACT, NPP, TPP, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
     if (e != cudaSuccess) return e;
     const int64_t per_cta = 2 * NPP;
