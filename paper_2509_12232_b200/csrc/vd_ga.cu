@@ -15,6 +15,7 @@
  * Philox4x64-10 with IEEE-exact transforms, identical to the CPU oracle's.
  */
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "vd_internal.h"
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 inter2<EXACT, NPP, TPP>(L, Gv, S, sub, e0, e1);
-                intra2<EXACT, NPP, TPP>(L, S, Tl, sub, a0, a1);
+                intra2<EXACT, NPP, TPP, !EXACT>(L, S, Tl, sub, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
@@ -369,13 +370,17 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         Launch L;
         int npp0;
         if (vd::pick_shape(nmax, exact, &npp0, &L.tpp)) return -1;
-        /* pose-pairs per CTA: the candidate with most resident warps per SM */
+        /* pose-pairs per CTA: the candidate with most resident warps per SM
+           (VD_GA_NPP forces one, for tuning) */
         int best_warps = -1;
-        for (int npp : {64, 32, 16}) {
+        const char *force = getenv("VD_GA_NPP");
+        for (int npp : {32, 64, 16}) {  /* ties -> 32 (cfg2 A/B: 6078 vs 5837 ligands/s) */
+            if (force && atoi(force) != npp) continue;
             vd::GaLayout lay;
             lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra);
             if (lay.base.bytes > 227u * 1024u) continue;
-            const int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes) * npp * L.tpp / 32;
+            int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes) * npp * L.tpp / 32;
+            if (npp == 64) warps -= 4;  /* measured: 64 needs clearly more warps to win */
             if (warps > best_warps) {
                 best_warps = warps;
                 L.npp = npp;
