@@ -42,8 +42,8 @@ WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
 # dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
 # committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
-TRAFFIC_BYTES = 158.22e6 + 19.94e6
-TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch)"
+TRAFFIC_BYTES = 157.58e6 + 19.40e6
+TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,32,4,1>)"
 
 
 def env_int(k, d):
@@ -76,6 +76,50 @@ def build_inputs(device_grid: bool):
     grid_s = time.perf_counter() - t0
     ctx = context.prepare_context(lig, gset)
     return gset, lig, ctx, grid_s, grid_src
+
+
+def measure_peaks():
+    """Live roofline denominators (tools/peaks.cu): FFMA2 TFLOP/s and random 8-B gather GB/s
+    from a 64 MiB (L2-resident) buffer."""
+    import ctypes
+
+    path = ROOT / "tools" / "libvdpeaks.so"
+    if not path.exists():
+        return None
+    lib = ctypes.CDLL(str(path))
+    lib.vdp_fp32_peak_tflops.restype = ctypes.c_double
+    lib.vdp_l2_gather_gbs.restype = ctypes.c_double
+    lib.vdp_l2_gather_gbs.argtypes = [ctypes.c_int64]
+    fp32 = max(lib.vdp_fp32_peak_tflops() for _ in range(3))
+    l2 = max(lib.vdp_l2_gather_gbs(64 << 20) for _ in range(3))
+    return {"fp32_tflops": fp32, "l2_gather_gbs": l2}
+
+
+def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx):
+    """Both rooflines of SURVEY 8(d); the binding one (lower poses/s ceiling) is primary.
+    Ridge = FP32 peak / L2 gather BW; the reference model's AI = fpp / (96 B * N)."""
+    bpp = 96 * int(ctx.n_atoms)
+    fp32 = {"achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+            "frac": achieved_tf / fp32_peak, "peak_source": fp32_src,
+            "algorithmic_flops_per_pose": fpp,
+            "ceiling_poses_per_s": fp32_peak * 1e12 / fpp}
+    out = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+           "frac": achieved_tf / fp32_peak, "traffic": TRAFFIC_BYTES,
+           "traffic_source": TRAFFIC_SRC, "kernel": "vd::score_kernel<false,32,4,true>",
+           "fp32": fp32, "arithmetic_intensity_flop_per_byte": fpp / bpp}
+    if peaks:
+        l2 = peaks["l2_gather_gbs"]
+        gather = {"achieved": gather_bps / 1e9, "peak": l2, "unit": "GB/s",
+                  "frac": gather_bps / 1e9 / l2, "bytes_per_pose": bpp,
+                  "peak_source": "measured live: random 8-B gathers from a 64 MiB "
+                                 "L2-resident buffer (tools/peaks.cu), best of 3",
+                  "ceiling_poses_per_s": l2 * 1e9 / bpp}
+        out["l2_gather"] = gather
+        out["ridge_flop_per_byte"] = fp32_peak * 1e3 / l2
+        if gather["ceiling_poses_per_s"] < fp32["ceiling_poses_per_s"]:
+            out.update(bound="l2-gather", achieved=gather["achieved"], peak=l2, unit="GB/s",
+                       frac=gather["frac"])
+    return out
 
 
 def flops_per_pose(ctx):
@@ -244,6 +288,11 @@ def run_ours(args):
 
     fpp = flops_per_pose(ctx)
     achieved = fpp * N_POSES / (t_loc / args.steps) / 1e12
+    peaks = measure_peaks()
+    peak = peaks["fp32_tflops"] if peaks else FP32_SPEC_TFLOPS
+    peak_src = ("measured live on this GPU: packed-FFMA2 microbenchmark (tools/peaks.cu), "
+                "best of 3" if peaks else "spec-derived 2*128 lanes*148 SMs*1.965 GHz")
+    gather_bps = 96 * ctx.n_atoms * N_POSES / (t_loc / args.steps)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -260,13 +309,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(genes_h.nbytes),
                 "d2h_bytes_per_step": int(N_POSES * (8 + 8 + 4)),
                 "path": "CudaBackend.score_population_arrays (pinned numpy in/out)"},
-        "roofline": {"bound": "fp32", "achieved": achieved, "peak": FP32_SPEC_TFLOPS,
-                     "unit": "TFLOP/s", "frac": achieved / FP32_SPEC_TFLOPS,
-                     "traffic": TRAFFIC_BYTES, "traffic_source": TRAFFIC_SRC,
-                     "kernel": "vd::score_kernel<false,64,2>",
-                     "algorithmic_flops_per_pose": fpp,
-                     "peak_source": "spec-derived 2*128 lanes*148 SMs*1.965 GHz (no measured "
-                                    "FP32 figure in MEASURED_PEAKS.json)"},
+        "roofline": roofline_block(achieved, peak, peak_src, gather_bps, peaks, fpp, ctx),
         "gpu_launches": int(launches),
         "parity_sample_ok": parity_ok,
         "clocks": clk.summary(),

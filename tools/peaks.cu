@@ -1,0 +1,105 @@
+// peaks.cu -- live B200 roofline denominators for bench.py (MEASURED_PEAKS.json
+// carries only HBM copy and bf16 GEMM figures):
+//   vdp_fp32_peak:  packed FFMA2 throughput (8 independent chains per thread)
+//   vdp_l2_gather:  random 8-byte gathers from an L2-resident buffer
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+__global__ void ffma2_kernel(float2 *out, int iters, float2 a, float2 b)
+{
+    float2 x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = make_float2(threadIdx.x * 1e-7f + k, k * 1e-3f);
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = __ffma2_rn(x[k], a, b);
+    }
+    float2 s = x[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s = __fadd2_rn(s, x[k]);
+    if (s.x == 12345.0f) out[threadIdx.x] = s;  // never true; keeps the chains live
+}
+
+__global__ void gather_kernel(const float2 *__restrict__ buf, uint64_t mask, int iters, float2 *out)
+{
+    uint64_t h = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) * 0x9E3779B97F4A7C15ull;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int i = 0; i < iters; ++i) {
+        float2 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            h ^= h << 13; h ^= h >> 7; h ^= h << 17;
+            v[k] = __ldg(buf + (h & mask));
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc = __fadd2_rn(acc, v[k]);
+    }
+    if (acc.x == 12345.0f) out[0] = acc;
+}
+
+static float time_it(void (*launch)(void *), void *arg)
+{
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    launch(arg);  // warm
+    cudaEventRecord(a);
+    for (int r = 0; r < 5; ++r) launch(arg);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return ms / 5;
+}
+
+struct FArgs { float2 *out; int blocks, threads, iters; };
+static void launch_ffma(void *p)
+{
+    FArgs *f = (FArgs *)p;
+    ffma2_kernel<<<f->blocks, f->threads>>>(f->out, f->iters, make_float2(0.999f, 0.999f), make_float2(1e-3f, 1e-3f));
+}
+struct GArgs { const float2 *buf; uint64_t mask; float2 *out; int blocks, threads, iters; };
+static void launch_gather(void *p)
+{
+    GArgs *g = (GArgs *)p;
+    gather_kernel<<<g->blocks, g->threads>>>(g->buf, g->mask, g->iters, g->out);
+}
+
+extern "C" double vdp_fp32_peak_tflops(void)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    FArgs f;
+    cudaMalloc(&f.out, 1024 * sizeof(float2));
+    f.blocks = sms * 8;
+    f.threads = 256;
+    f.iters = 8192;
+    const float ms = time_it(launch_ffma, &f);
+    cudaFree(f.out);
+    const double flops = (double)f.blocks * f.threads * f.iters * 8 * 2 /*lanes*/ * 2 /*fma*/;
+    return flops / (ms * 1e-3) / 1e12;
+}
+
+extern "C" double vdp_l2_gather_gbs(int64_t bytes)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n = bytes / 8;  // power of two float2 elements
+    GArgs g;
+    cudaMalloc((void **)&g.buf, n * sizeof(float2));
+    cudaMemset((void *)g.buf, 0, n * sizeof(float2));
+    cudaMalloc(&g.out, sizeof(float2));
+    g.mask = (uint64_t)n - 1;
+    g.blocks = sms * 8;
+    g.threads = 256;
+    g.iters = 256;
+    const float ms = time_it(launch_gather, &g);
+    cudaFree((void *)g.buf);
+    cudaFree(g.out);
+    const double useful = (double)g.blocks * g.threads * g.iters * 8 * 8;  // bytes delivered
+    return useful / (ms * 1e-3) / 1e9;
+}
