@@ -273,6 +273,7 @@ cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const Li
     VD_G(false, 64, 1); VD_G(false, 32, 1); VD_G(false, 16, 1);
     VD_G(false, 64, 2); VD_G(false, 32, 2); VD_G(false, 16, 2);
     VD_G(false, 64, 4); VD_G(false, 32, 4); VD_G(false, 16, 4);
+    VD_G(false, 32, 8); VD_G(false, 16, 8);
 #undef VD_G
     return cudaErrorInvalidConfiguration;
 }
@@ -302,6 +303,7 @@ int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes)
     VD_O(false, 64, 1); VD_O(false, 32, 1); VD_O(false, 16, 1);
     VD_O(false, 64, 2); VD_O(false, 32, 2); VD_O(false, 16, 2);
     VD_O(false, 64, 4); VD_O(false, 32, 4); VD_O(false, 16, 4);
+    VD_O(false, 32, 8); VD_O(false, 16, 8);
 #undef VD_O
     return 0;
 }

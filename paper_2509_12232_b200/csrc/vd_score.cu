@@ -91,11 +91,13 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
 int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
 {
     const unsigned limit = 200 * 1024;
-    int t = exact ? 1 : (n_atoms <= 16 ? 1 : 4);
+    /* threads per pose pair: more subs for larger ligands, where 12*N bytes of
+       shared memory per pose leave few poses (and warps) per SM */
+    int t = exact ? 1 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 4 : 8));
     if (!exact)
         if (const char *ov = getenv("VD_TPP")) {  /* tuning override: 1, 2 or 4 */
             const int v = atoi(ov);
-            if (v == 1 || v == 2 || v == 4) t = v;
+            if (v == 1 || v == 2 || v == 4 || v == 8) t = v;
         }
     int force_npp = 0;
     if (!exact)
@@ -153,6 +155,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
     VD_L(false, 64, 1); VD_L(false, 32, 1); VD_L(false, 16, 1);
     VD_L(false, 64, 2); VD_L(false, 32, 2); VD_L(false, 16, 2);
     VD_L(false, 64, 4); VD_L(false, 32, 4); VD_L(false, 16, 4);
+    VD_L(false, 32, 8); VD_L(false, 16, 8);
 #undef VD_L
     return cudaErrorInvalidConfiguration;
 }

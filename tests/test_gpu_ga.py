@@ -173,3 +173,42 @@ def test_exact_batch_matches_oracle_dock_many(cuda):
         G = 7 + ligs[i][1].n_torsions
         assert np.array_equal(e.result.best_genotype, g[i, :G])
         assert e.result.best_score.total == float(bt[i])
+
+
+def test_cfg4_ligand_exact_ga_matches_oracle(cuda):
+    """128-atom / 32-torsion ligand (cfg4 shape): device GA == oracle GA, bit for bit."""
+    from paper_2509_12232_b200 import hostprep
+    from paper_2509_12232_b200.context import prepare_context
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    c = fx.pop_case("cfg1")
+    topo = hostprep.TopologyBatch.synth(4, 7, 1).topology(0)
+    ctx = prepare_context(topo, c["grid"])
+    cfg = GaConfig(population_size=24, generations=3, seed=1)
+    res = dock(topo, c["grid"], cfg, backend=cuda["exact"], context=ctx)
+    lo, hi = c["grid"].spec.origin, c["grid"].spec.upper
+    g, bt, *_, trace, ne = oracle.dock(oracle.Ligand(ctx), oracle.ga_params(cfg, lo, hi), 1, 0)
+    assert np.array_equal(res.trace.view(np.uint32), trace.view(np.uint32))
+    assert np.array_equal(res.best_genotype, g)
+
+
+def test_screen_batch_records_failures_in_place(cuda):
+    """A ligand whose atom type has no map fails alone (vd/screening.py:195-244)."""
+    from paper_2509_12232_b200 import synth
+    from paper_2509_12232_b200.ga import GaConfig
+    from paper_2509_12232_b200.screening import ScreenConfig, screen_batch
+    from paper_2509_12232_b200.topology import LigandTopology
+
+    c = fx.pop_case("cfg1")
+    good = synth.config_ligand(2, 3)
+    bad = LigandTopology(good.coords0, np.full(good.n_atoms, fx.TABLE.index_of("S")),
+                         good.charge, good.bonds, good.rotatable_bonds)
+    maps = {k: v for k, v in c["grid"].maps.items() if k != "S"}
+    from paper_2509_12232_b200 import gridmaps
+
+    g = gridmaps.GridMapSet(c["grid"].spec, maps)
+    out = screen_batch([("a", good), ("b", bad), ("c", good)], g,
+                       ScreenConfig(ga=GaConfig(population_size=16, generations=3)))
+    assert out[0].error is None and out[2].error is None
+    assert out[1].result is None and "no map" in out[1].error
+    assert out[0].seed_key == (0, 0) and out[2].seed_key == (0, 2)

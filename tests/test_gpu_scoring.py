@@ -237,3 +237,33 @@ def test_grid_builder_vs_reference(case):
         g = got.maps[label].astype(np.float64)
         rel = np.abs(g - w) / np.maximum(np.abs(w), 1e-4)
         assert rel.max() < 1e-4, (label, rel.max())
+
+
+@pytest.mark.parametrize("name", ["cfg1", "big"])
+def test_fast_mode_plain_grid_layout(cuda, name, monkeypatch):
+    """The unpacked (n_maps, nx, ny, nz) gather path (used when the packed copy would
+    not stay L2-resident, e.g. cfg4's 126^3 grid) agrees like the packed one."""
+    from paper_2509_12232_b200 import gridmaps
+    from paper_2509_12232_b200.backend import CudaBackend
+    from paper_2509_12232_b200.context import prepare_context
+
+    monkeypatch.setenv("VD_NO_PACK", "1")
+    c = fx.pop_case(name)
+    g2 = gridmaps.GridMapSet(c["grid"].spec, dict(c["grid"].maps))  # fresh device grid
+    ctx = prepare_context(c["topo"], g2)
+    b = CudaBackend(mode="fast", device=0)
+    e, a, t = b.score_population_arrays(c["genes"], ctx)
+    assert fx.within_tol(t, c["total"]).all()
+    assert fx.within_tol(e, c["inter"]).all()
+
+
+@pytest.mark.parametrize("tpp", ["1", "2", "4", "8"])
+def test_fast_mode_every_launch_shape(cuda, tpp, monkeypatch):
+    """Every threads-per-pose-pair shape gives the same poses and in-tolerance energies."""
+    from paper_2509_12232_b200.backend import CudaBackend
+
+    monkeypatch.setenv("VD_TPP", tpp)
+    c = fx.pop_case("big")
+    b = CudaBackend(mode="fast", device=0)
+    e, a, t = b.score_population_arrays(c["genes"], c["ctx"])
+    assert fx.within_tol(t, c["total"]).all()
