@@ -212,3 +212,21 @@ def test_screen_batch_records_failures_in_place(cuda):
     assert out[0].error is None and out[2].error is None
     assert out[1].result is None and "no map" in out[1].error
     assert out[0].seed_key == (0, 0) and out[2].seed_key == (0, 2)
+
+
+@pytest.mark.parametrize("kw", [dict(elitism_count=3, tournament_size=3),
+                                dict(elitism_count=0, tournament_size=1, crossover_rate=0.0),
+                                dict(mutation_rate=0.3, crossover_rate=1.0, population_size=33),
+                                dict(population_size=2, generations=4)])
+def test_exact_ga_operator_variants_match_oracle(cuda, kw):
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    c = fx.pop_case("refgen")
+    base = dict(population_size=40, generations=6, seed=13)
+    base.update(kw)
+    cfg = GaConfig(**base)
+    res = dock(c["topo"], c["grid"], cfg, backend=cuda["exact"], context=c["ctx"])
+    g, bt, *_, trace, ne = _oracle_dock(c, cfg, 13)
+    assert np.array_equal(res.trace.view(np.uint32), trace.view(np.uint32))
+    assert np.array_equal(res.best_genotype, g)
+    assert res.n_evaluations == ne
