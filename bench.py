@@ -316,6 +316,16 @@ def run_ours(args):
     }
     if args.screen_ligands > 0:
         line["screening"] = screening_leg(args, rank, world, dist, dev)
+        if not args.csv:
+            line["screening"].pop("_modeled", None)
+        if args.csv and rank == 0:
+            from paper_2509_12232_b200 import benchrecords as br
+
+            s = line["screening"]
+            fl, by = s.pop("_modeled")
+            rec = br.make_record(s["workload"], "cuda", [s["ms"]], s["ligands"], fl, by,
+                                 threads=world)
+            br.emit_csv([rec], args.csv)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(ctx, genes_h, args.cpu_seconds)
     if rank == 0:
@@ -371,13 +381,19 @@ def screening_leg(args, rank, world, dist, dev):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     evals = n * ga.population_size * (ga.generations + 1)
+    from paper_2509_12232_b200 import benchrecords as br
+
+    npairs = float(arrays["pair_start"][-1]) / max(1, count)
+    modeled = br.modeled_work(npairs * n, float(batch.n_atoms.mean()) * n, ga.population_size,
+                              ga.generations)
     return {"metric": "ligands docked/sec", "value": n / t_max, "unit": "ligands/s",
             "pose_evals_per_s": evals / t_max, "ligands": n, "ms": 1e3 * t_max,
             "ga": "pop 256 x 200 generations (cfg2 distribution, 64^3 grid, 3000-atom receptor)",
             "workload": "cfg2-screen-10k" if n == 10000 else f"cfg2-distribution x{n}",
             "gathered_records": int(rec.shape[0]), "gather_ms": round(1e3 * t_gather, 3),
             "host_prep_s_per_rank": round(prep_s, 3),
-            "timing": "CUDA events around the one persistent GA launch, max over ranks"}
+            "timing": "CUDA events around the one persistent GA launch, max over ranks",
+            "_modeled": modeled}
 
 
 def cpu_baseline(ctx, genes, seconds=10.0):
@@ -448,6 +464,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=16384)
+    ap.add_argument("--csv", default=None, help="also write a BenchRecord CSV row (vd/bench.py schema)")
     ap.add_argument("--screen-ligands", type=int, default=10000,
                     help="cfg2 ligands for the ligands/s leg (0 disables)")
     args = ap.parse_args()

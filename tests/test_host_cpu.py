@@ -253,3 +253,24 @@ def test_ring_bond_not_rotatable():
                                 (topology.RotatableBond(0, 1, np.empty(0, np.int32)),))
     with pytest.raises(ValueError, match="lies on a ring"):
         topology.build_fragment_masks(t)
+
+
+def test_bench_records_csv_byte_stable_and_parseable():
+    """vd/bench.py:322-341 CSV rules; columns == the reference's BenchRecord fields."""
+    from paper_2509_12232_b200 import benchrecords as br
+
+    fl, by = br.modeled_work(608, 40, 256, 200)
+    assert fl == 256 * 200 * (32 * 608 + 107 * 40)
+    recs = [br.make_record("cfg2", "cuda", [2.0, 1.0, 1.1, 0.9], 10, fl, by, warmup_discard=1),
+            br.make_record("cfg2", "reference", [500.0, 400.0], 10, fl, by)]
+    br.fill_speedups(recs)
+    assert recs[0].speedup_vs_reference == pytest.approx(450.0 / 1.0)
+    a = br.emit_csv(recs)
+    b = br.emit_csv(list(reversed(recs)))
+    assert a == b and a.splitlines()[0].split(",") == br.BENCH_CSV_COLUMNS
+    assert br.BENCH_CSV_COLUMNS == ["scenario", "backend", "threads", "mean_ms", "stddev_ms", "cv",
+                                    "ligands_per_s", "modeled_flops", "modeled_bytes",
+                                    "modeled_ai", "speedup_vs_reference", "n_samples",
+                                    "lane_utilization", "status"]
+    back = br.parse_csv(a)
+    assert br.emit_csv(back) == a
