@@ -51,22 +51,26 @@ bool is_device_ptr(const void *p)
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-__global__ void pack_zpairs(const float *__restrict__ maps, int64_t n, int nz, float2 *zp)
+__global__ void pack_yz(const float *__restrict__ maps, int64_t n, int ny, int nz, float4 *yz)
 {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
-        const bool last = (k % nz) == nz - 1;
-        zp[k] = make_float2(maps[k], last ? 0.0f : maps[k + 1]);
+        const bool zl = (k % nz) == nz - 1, yl = ((k / nz) % ny) == ny - 1;
+        yz[k] = make_float4(maps[k], zl ? 0.f : maps[k + 1], yl ? 0.f : maps[k + nz],
+                            (zl || yl) ? 0.f : maps[k + nz + 1]);
     }
 }
 
 __global__ void pack_ed(const float *__restrict__ e, const float *__restrict__ d, int64_t n,
-                        int nz, float4 *ed)
+                        int ny, int nz, float4 *ed)
 {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
-        const bool last = (k % nz) == nz - 1;
-        ed[k] = make_float4(e[k], last ? 0.0f : e[k + 1], d[k], last ? 0.0f : d[k + 1]);
+        const bool zl = (k % nz) == nz - 1, yl = ((k / nz) % ny) == ny - 1;
+        ed[2 * k] = make_float4(e[k], zl ? 0.f : e[k + 1], yl ? 0.f : e[k + nz],
+                                (zl || yl) ? 0.f : e[k + nz + 1]);
+        ed[2 * k + 1] = make_float4(d[k], zl ? 0.f : d[k + 1], yl ? 0.f : d[k + nz],
+                                    (zl || yl) ? 0.f : d[k + nz + 1]);
     }
 }
 
@@ -74,27 +78,27 @@ __global__ void pack_ed(const float *__restrict__ e, const float *__restrict__ d
 bool make_packed(vd_grid *g)
 {
     const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
-    const int64_t bytes = nodes * (8 * (int64_t)g->n_maps + 16);
+    const int64_t bytes = nodes * (16 * (int64_t)g->n_maps + 32);
     if (getenv("VD_NO_PACK") || bytes > (int64_t)96 << 20) return true;
-    if (!check(cudaMalloc(&g->d_zp, sizeof(float2) * nodes * g->n_maps), "alloc zp")) return false;
-    pack_zpairs<<<1184, 256>>>(g->d_maps, nodes * g->n_maps, g->nz, g->d_zp);
-    return check(cudaGetLastError(), "pack zp") && check(cudaDeviceSynchronize(), "pack zp sync");
+    if (!check(cudaMalloc(&g->d_yz, sizeof(float4) * nodes * g->n_maps), "alloc yz")) return false;
+    pack_yz<<<1184, 256>>>(g->d_maps, nodes * g->n_maps, g->ny, g->nz, g->d_yz);
+    return check(cudaGetLastError(), "pack yz") && check(cudaDeviceSynchronize(), "pack yz sync");
 }
 
 static const float4 *ed_for(const vd_grid *gc, int e, int d)
 {
     vd_grid *g = const_cast<vd_grid *>(gc);
-    if (!g->d_zp || e < 0 || d < 0 || e >= g->n_maps || d >= g->n_maps) return nullptr;
+    if (!g->d_yz || e < 0 || d < 0 || e >= g->n_maps || d >= g->n_maps) return nullptr;
     std::lock_guard<std::mutex> lk(g->ed_lock);
     auto it = g->d_ed.find({e, d});
     if (it != g->d_ed.end()) return it->second;
     const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
     float4 *p = nullptr;
-    if (cudaMalloc(&p, sizeof(float4) * nodes) != cudaSuccess) {
+    if (cudaMalloc(&p, 2 * sizeof(float4) * nodes) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
-    pack_ed<<<1184, 256>>>(g->d_maps + nodes * e, g->d_maps + nodes * d, nodes, g->nz, p);
+    pack_ed<<<1184, 256>>>(g->d_maps + nodes * e, g->d_maps + nodes * d, nodes, g->ny, g->nz, p);
     if (cudaDeviceSynchronize() != cudaSuccess) {
         cudaGetLastError();
         cudaFree(p);
@@ -108,7 +112,7 @@ vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)
 {
     vd::GridView v;
     v.ed = ed_for(g, elec_map, desolv_map);
-    v.zp = v.ed ? g->d_zp : nullptr;
+    v.yz = v.ed ? g->d_yz : nullptr;
     v.maps = g->d_maps;
     v.nx = g->nx;
     v.ny = g->ny;
@@ -247,7 +251,7 @@ int vd_grid_destroy(vd_grid *g)
 {
     if (!g) return 0;
     cudaFree(g->d_maps);
-    cudaFree(g->d_zp);
+    cudaFree(g->d_yz);
     for (auto &kv : g->d_ed) cudaFree(kv.second);
     delete g;
     return 0;
@@ -442,7 +446,8 @@ static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const vo
     }
     /* chunked two-stream pipeline through device staging buffers */
     vdi::Pipe *pp = vdi::pipe_for_device();
-    const int64_t CH = std::min<int64_t>(P, 1 << 17);
+    static const int64_t chunk_env = getenv("VD_CHUNK") ? atoll(getenv("VD_CHUNK")) : 0;
+    const int64_t CH = std::min<int64_t>(P, chunk_env > 0 ? chunk_env : (1 << 17));
     char *d_in[2] = {nullptr, nullptr};
     double *d_e[2] = {nullptr, nullptr}, *d_a[2] = {nullptr, nullptr};
     float *d_t[2] = {nullptr, nullptr};

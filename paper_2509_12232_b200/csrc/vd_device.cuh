@@ -38,10 +38,12 @@ struct GridView {
     int64_t mstride;        /* nx * ny * nz */
     float lo0, lo1, lo2, hi0, hi1, hi2, spacing;
     /* packed gather layout (null when the packed copy would not stay L2-resident):
-     *   zp[m][node] = (v[node], v[node + 1])           z-pair of every map, 8 B
-     *   ed[node]    = (e[n], e[n+1], d[n], d[n+1])      elec + desolv z-pairs, 16 B
-     * -> 4 LDG.64 + 4 LDG.128 per atom instead of 24 scalar gathers */
-    const float2 *zp;
+     *   yz[m][node]  = (v[y,z], v[y,z+1], v[y+1,z], v[y+1,z+1])   yz-brick, 16 B
+     *   ed[2*node]   = elec yz-brick, ed[2*node+1] = desolv yz-brick (32 B, one LDG.256)
+     * -> 2 LDG.128 + 2 LDG.256 per atom instead of 24 scalar gathers: each
+     *    scattered warp-wide load costs ~one L1TEX wavefront per lane, so the
+     *    gather cost scales with load instructions, not bytes */
+    const float4 *yz;
     const float4 *ed;
 };
 
@@ -308,8 +310,9 @@ __device__ __forceinline__ float trilerp(const float *__restrict__ m, int idx, i
 struct Gather {
     float fx, fy, fz, pterm;
     bool inb;
-    float2 t[4];   /* type map z-pairs at (x,y) corners 00, 01, 10, 11 */
-    float4 ed[4];  /* elec/desolv z-pairs */
+    float4 t[2];   /* type-map yz-bricks at x and x+1 */
+    float4 e[2];   /* elec yz-bricks */
+    float4 d[2];   /* desolv yz-bricks */
 };
 
 __device__ __forceinline__ void cell_of(const GridView &G, float x, float y, float z, float pen,
@@ -332,18 +335,22 @@ __device__ __forceinline__ void cell_of(const GridView &G, float x, float y, flo
     idx = (ix * G.ny + iy) * G.nz + iz;
 }
 
-__device__ __forceinline__ void issue_packed(const GridView &G, const float2 *__restrict__ tz,
+__device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z),
+          "=f"(hi.w)
+        : "l"(p));
+}
+
+__device__ __forceinline__ void issue_packed(const GridView &G, const float4 *__restrict__ ty,
                                              int idx, Gather &g)
 {
-    const int nz = G.nz, nyz = G.ny * G.nz;
-    g.t[0] = __ldg(tz + idx);
-    g.t[1] = __ldg(tz + idx + nz);
-    g.t[2] = __ldg(tz + idx + nyz);
-    g.t[3] = __ldg(tz + idx + nyz + nz);
-    g.ed[0] = __ldg(G.ed + idx);
-    g.ed[1] = __ldg(G.ed + idx + nz);
-    g.ed[2] = __ldg(G.ed + idx + nyz);
-    g.ed[3] = __ldg(G.ed + idx + nyz + nz);
+    const int nyz = G.ny * G.nz;
+    g.t[0] = __ldg(ty + idx);
+    g.t[1] = __ldg(ty + idx + nyz);
+    ld256(G.ed + 2 * (int64_t)idx, g.e[0], g.d[0]);
+    ld256(G.ed + 2 * (int64_t)(idx + nyz), g.e[1], g.d[1]);
 }
 
 /* trilinear value from the 8 corners, the reference's collapse order and rounding:
@@ -358,14 +365,18 @@ __device__ __forceinline__ float tri8(float v000, float v001, float v010, float 
     return lerp_<true>(c0, c1, fz);
 }
 
+__device__ __forceinline__ float tri_b(const float4 &b0, const float4 &b1, float fx, float fy,
+                                       float fz)
+{
+    /* brick (v[y,z], v[y,z+1], v[y+1,z], v[y+1,z+1]) at x (b0) and x+1 (b1) */
+    return tri8(b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, fx, fy, fz);
+}
+
 __device__ __forceinline__ float finish_packed(const Gather &g, float q, float dsf)
 {
-    const float vt = tri8(g.t[0].x, g.t[0].y, g.t[1].x, g.t[1].y, g.t[2].x, g.t[2].y, g.t[3].x,
-                          g.t[3].y, g.fx, g.fy, g.fz);
-    const float ve = tri8(g.ed[0].x, g.ed[0].y, g.ed[1].x, g.ed[1].y, g.ed[2].x, g.ed[2].y,
-                          g.ed[3].x, g.ed[3].y, g.fx, g.fy, g.fz);
-    const float vd = tri8(g.ed[0].z, g.ed[0].w, g.ed[1].z, g.ed[1].w, g.ed[2].z, g.ed[2].w,
-                          g.ed[3].z, g.ed[3].w, g.fx, g.fy, g.fz);
+    const float vt = tri_b(g.t[0], g.t[1], g.fx, g.fy, g.fz);
+    const float ve = tri_b(g.e[0], g.e[1], g.fx, g.fy, g.fz);
+    const float vd = tri_b(g.d[0], g.d[1], g.fx, g.fy, g.fz);
     const float gterm = __fadd_rn(__fadd_rn(vt, __fmul_rn(q, ve)), __fmul_rn(dsf, vd));
     return g.inb ? gterm : g.pterm;
 }
@@ -396,14 +407,14 @@ template <bool EXACT, int NPP, int TPP>
 __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, const float2 *S,
                                        int sub, double &e0, double &e1)
 {
-    if (G.zp != nullptr && !EXACT) {
+    if (G.yz != nullptr && !EXACT) {
         const int n = L.n_atoms;
         int i = sub;
         if (i >= n) return;
         Gather c0, c1;
         {
             const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
-            const float2 *tz = G.zp + G.mstride * __float_as_int(L.atom2[i].y);
+            const float4 *tz = G.yz + G.mstride * __float_as_int(L.atom2[i].y);
             int idx0, idx1;
             cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0);
             cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1);
@@ -415,7 +426,7 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
             Gather n0, n1;
             if (in < n) {
                 const float2 x = VD_S2(in, 0), y = VD_S2(in, 1), z = VD_S2(in, 2);
-                const float2 *tz = G.zp + G.mstride * __float_as_int(L.atom2[in].y);
+                const float4 *tz = G.yz + G.mstride * __float_as_int(L.atom2[in].y);
                 int idx0, idx1;
                 cell_of(G, x.x, y.x, z.x, L.penalty, n0, idx0);
                 cell_of(G, x.y, y.y, z.y, L.penalty, n1, idx1);

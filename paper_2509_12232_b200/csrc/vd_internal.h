@@ -16,7 +16,7 @@ struct vd_grid {
     int n_maps, nx, ny, nz;
     float lo[3], hi[3], spacing;
     float *d_maps;           /* (n_maps, nx, ny, nz) */
-    float2 *d_zp;            /* packed z-pairs of every map, or null (see GridView) */
+    float4 *d_yz;            /* packed yz-bricks of every map, or null (see GridView) */
     std::mutex ed_lock;
     std::map<std::pair<int, int>, float4 *> d_ed;  /* packed (elec, desolv) per map pair */
 };
