@@ -475,6 +475,9 @@ __device__ __forceinline__ float pair_exact(float dx, float dy, float dz, bool h
     return __fadd_rn(__fadd_rn(well, elec), des);
 }
 
+#ifndef VD_DESOLV_POLY
+#define VD_DESOLV_POLY 0
+#endif
 /* 2^x for x <= 0 on the FMA pipe (keeps the MUFU pipe for rsqrt/ex2/rcp):
  * n = rint(x) via the 1.5*2^23 magic add, f = x - n in [-1/2, 1/2], degree-5
  * fit of 2^f (max rel err 3e-7), 2^n assembled in the exponent field. */
@@ -517,7 +520,11 @@ __device__ __forceinline__ float2 pair_fast2(float2 dx, float2 dy, float2 dz, fl
     const float2 rc = f2(mufu_rcp(dd.x), mufu_rcp(dd.y));
     const float2 elec = fmul2(fmul2(f2(cf.z), den), rc);
     const float2 darg = fmul2(r2, f2((float)(-1.4426950408889634 / kDesolvDenom)));
+#if VD_DESOLV_POLY
     const float2 des = fmul2(f2(cf.w), exp2_poly2(darg));
+#else
+    const float2 des = fmul2(f2(cf.w), f2(mufu_ex2(darg.x), mufu_ex2(darg.y)));
+#endif
     float2 t = fadd2(fadd2(well, elec), des);
     if (CUT) {
         t.x = r2.x > cut2 ? 0.0f : t.x;
@@ -549,17 +556,16 @@ __device__ __forceinline__ float2 row_fast(const float2 *S, int i, int kb, int k
 constexpr int kFlatUnroll = VD_FLAT_UNROLL;
 template <int NPP, int TPP, bool HB, bool CUT>
 __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, const float4 *tc,
-                                            const int *tij, int sub, float cut2)
+                                            const int2 *toff, int sub, float cut2)
 {
     float2 acc = f2(0.0f);
 #pragma unroll kFlatUnroll
     for (int k = kb + sub; k < ke; k += TPP) {
         const float4 c = tc[k];
-        const int w = tij[k];
-        const int i = w & 0xffff, j = w >> 16;
-        acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(VD_S2(i, 0), VD_S2(j, 0)),
-                                             fsub2(VD_S2(i, 1), VD_S2(j, 1)),
-                                             fsub2(VD_S2(i, 2), VD_S2(j, 2)), c, cut2));
+        const int2 o = toff[k];  /* element offsets 3*NPP*i, 3*NPP*j into the pose tile */
+        const float2 *Si = S + o.x, *Sj = S + o.y;
+        acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(Si[0], Sj[0]), fsub2(Si[NPP], Sj[NPP]),
+                                             fsub2(Si[2 * NPP], Sj[2 * NPP]), c, cut2));
     }
     return acc;
 }
@@ -569,6 +575,7 @@ struct PairTile {
     float4 *coef;   /* [kTile] */
     int *j;         /* [kTile] fast: j; exact: packed ij */
     int4 *row;      /* [kTile] fast rows of the tile */
+    int2 *off;      /* [kTile] flat: pose-tile element offsets of i and j */
 };
 
 /* intra of both poses over this sub's share of the pairs (all CTA threads must call) */
@@ -651,15 +658,16 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
                 if (tid == 0) s_kh = cnt;
                 for (int r = tid; r < r1 - r0; r += B) {
                     const int4 row = T.row[r];
-                    for (int k = row.y - k0; k < row.z - k0; ++k) T.j[k] |= row.x;
+                    for (int k = row.y - k0; k < row.z - k0; ++k)
+                        T.off[k] = make_int2(3 * NPP * row.x, 3 * NPP * (T.j[k] >> 16));
                     if (row.w && (r == 0 || !T.row[r - 1].w)) s_kh = row.y - k0;
                 }
                 __syncthreads();
                 const int kh = s_kh;
-                part = cut ? flat_fast<NPP, TPP, false, true>(S, 0, kh, T.coef, T.j, sub, L.cut2)
-                           : flat_fast<NPP, TPP, false, false>(S, 0, kh, T.coef, T.j, sub, L.cut2);
-                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, cnt, T.coef, T.j, sub, L.cut2)
-                                       : flat_fast<NPP, TPP, true, false>(S, kh, cnt, T.coef, T.j, sub, L.cut2));
+                part = cut ? flat_fast<NPP, TPP, false, true>(S, 0, kh, T.coef, T.off, sub, L.cut2)
+                           : flat_fast<NPP, TPP, false, false>(S, 0, kh, T.coef, T.off, sub, L.cut2);
+                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, cnt, T.coef, T.off, sub, L.cut2)
+                                       : flat_fast<NPP, TPP, true, false>(S, kh, cnt, T.coef, T.off, sub, L.cut2));
             } else
             for (int r = 0; r < r1 - r0; ++r) {
                 const int4 row = T.row[r];
@@ -710,7 +718,7 @@ __device__ __forceinline__ void reduce_subs(double *red, int pp, int sub, double
 /* Dynamic shared-memory layout of the scoring CTAs. */
 struct SmemLayout {
     unsigned topo_atom, topo_atom2, topo_tors, topo_frag, scratch;
-    unsigned tile_coef, tile_j, tile_row, red, extra, bytes;
+    unsigned tile_coef, tile_j, tile_row, tile_off, red, extra, bytes;
 };
 
 __host__ __device__ inline unsigned align16(unsigned v) { return (v + 15u) & ~15u; }
@@ -731,7 +739,7 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     /* pose-build scratch aliases the pair tiles (the pose is built before intra
        stages pairs; build_pose2 syncs before its first scratch write) */
     const unsigned scratch_bytes = (tpp > 1) ? 4u * kPoseScratch * (unsigned)npp : 0u;
-    if (!alias || scratch_bytes > 36u * kTile) {
+    if (!alias || scratch_bytes > 44u * kTile) {
         s.scratch = off;
         off = align16(off + scratch_bytes);
     } else {
@@ -743,9 +751,12 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     off += 16u * kTile;
     s.tile_j = off;
     off += 4u * kTile;
+    off = align16(off);
+    s.tile_off = off;
+    off += 8u * kTile;
     /* sub reduction reuses the pair tiles (intra is finished when it runs) */
     const unsigned red_bytes = (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
-    if (red_bytes <= 36u * kTile) {
+    if (red_bytes <= 44u * kTile) {
         s.red = s.tile_coef;
     } else {
         s.red = off;

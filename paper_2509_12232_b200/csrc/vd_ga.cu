@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     PairTile Tl{reinterpret_cast<float4 *>(smem + lay.base.tile_coef),
                 reinterpret_cast<int *>(smem + lay.base.tile_j),
-                reinterpret_cast<int4 *>(smem + lay.base.tile_row)};
+                reinterpret_cast<int4 *>(smem + lay.base.tile_row),
+                reinterpret_cast<int2 *>(smem + lay.base.tile_off)};
     double *red = reinterpret_cast<double *>(smem + lay.base.red);
     float *fit = reinterpret_cast<float *>(smem + lay.off_fit);
     double *e64 = reinterpret_cast<double *>(smem + lay.off_e);

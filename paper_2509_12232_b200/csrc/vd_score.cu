@@ -28,7 +28,8 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     PairTile T{reinterpret_cast<float4 *>(smem + lay.tile_coef),
                reinterpret_cast<int *>(smem + lay.tile_j),
-               reinterpret_cast<int4 *>(smem + lay.tile_row)};
+               reinterpret_cast<int4 *>(smem + lay.tile_row),
+               reinterpret_cast<int2 *>(smem + lay.tile_off)};
     const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
                                      lay.topo_frag);
     __syncthreads();
