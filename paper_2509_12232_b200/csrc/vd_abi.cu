@@ -18,6 +18,10 @@
 
 #include "vd_internal.h"
 
+#ifndef VD_TYPE_ZPAIR
+#define VD_TYPE_ZPAIR 1
+#endif
+
 namespace vd {
 cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
                          const double *genes, const float *poses, int64_t P, int ngenes,
@@ -61,6 +65,15 @@ __global__ void pack_yz(const float *__restrict__ maps, int64_t n, int ny, int n
     }
 }
 
+__global__ void pack_z(const float *__restrict__ maps, int64_t n, int nz, float2 *zp)
+{
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const bool zl = (k % nz) == nz - 1;
+        zp[k] = make_float2(maps[k], zl ? 0.f : maps[k + 1]);
+    }
+}
+
 __global__ void pack_ed(const float *__restrict__ e, const float *__restrict__ d, int64_t n,
                         int ny, int nz, float4 *ed)
 {
@@ -78,11 +91,15 @@ __global__ void pack_ed(const float *__restrict__ e, const float *__restrict__ d
 bool make_packed(vd_grid *g)
 {
     const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
-    const int64_t bytes = nodes * (16 * (int64_t)g->n_maps + 32);
+    const int64_t bytes = nodes * ((VD_TYPE_ZPAIR ? 8 : 16) * (int64_t)g->n_maps + 32);
     if (getenv("VD_NO_PACK") || bytes > (int64_t)96 << 20) return true;
-    if (!check(cudaMalloc(&g->d_yz, sizeof(float4) * nodes * g->n_maps), "alloc yz")) return false;
-    pack_yz<<<1184, 256>>>(g->d_maps, nodes * g->n_maps, g->ny, g->nz, g->d_yz);
-    return check(cudaGetLastError(), "pack yz") && check(cudaDeviceSynchronize(), "pack yz sync");
+    /* type maps are packed lazily in ed_for(): only the maps a ligand set can
+       reference (every map except its elec/desolv pair).  Type maps use z-pairs
+       (8 B/node), not yz-bricks (16 B/node): at cfg1 the brick copy (74 MB touched)
+       thrashed L2 (834 MB DRAM read per 1M-pose launch vs 168 MB with z-pairs,
+       and 1.7% slower) - profiles/r1_score_kernel.md */
+    g->yz_packed.assign(g->n_maps, 0);
+    return check(cudaMalloc(&g->d_yz, (VD_TYPE_ZPAIR ? sizeof(float2) : sizeof(float4)) * nodes * g->n_maps), "alloc yz");
 }
 
 static const float4 *ed_for(const vd_grid *gc, int e, int d)
@@ -99,6 +116,16 @@ static const float4 *ed_for(const vd_grid *gc, int e, int d)
         return nullptr;
     }
     pack_ed<<<1184, 256>>>(g->d_maps + nodes * e, g->d_maps + nodes * d, nodes, g->ny, g->nz, p);
+    for (int m = 0; m < g->n_maps; ++m)
+        if (m != e && m != d && !g->yz_packed[m]) {
+#if VD_TYPE_ZPAIR
+            pack_z<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->nz,
+                                  reinterpret_cast<float2 *>(g->d_yz) + nodes * m);
+#else
+            pack_yz<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->ny, g->nz, g->d_yz + nodes * m);
+#endif
+            g->yz_packed[m] = 1;
+        }
     if (cudaDeviceSynchronize() != cudaSuccess) {
         cudaGetLastError();
         cudaFree(p);

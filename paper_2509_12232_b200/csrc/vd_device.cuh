@@ -38,9 +38,10 @@ struct GridView {
     int64_t mstride;        /* nx * ny * nz */
     float lo0, lo1, lo2, hi0, hi1, hi2, spacing;
     /* packed gather layout (null when the packed copy would not stay L2-resident):
-     *   yz[m][node]  = (v[y,z], v[y,z+1], v[y+1,z], v[y+1,z+1])   yz-brick, 16 B
+     *   yz[m][node]  = (v[z], v[z+1])  z-pair, 8 B (VD_TYPE_ZPAIR=1, default), or the
+     *                  yz-brick (v[y,z], v[y,z+1], v[y+1,z], v[y+1,z+1]), 16 B (=0)
      *   ed[2*node]   = elec yz-brick, ed[2*node+1] = desolv yz-brick (32 B, one LDG.256)
-     * -> 2 LDG.128 + 2 LDG.256 per atom instead of 24 scalar gathers: each
+     * -> 4 LDG.64 + 2 LDG.256 per atom instead of 24 scalar gathers: each
      *    scattered warp-wide load costs ~one L1TEX wavefront per lane, so the
      *    gather cost scales with load instructions, not bytes */
     const float4 *yz;
@@ -310,7 +311,7 @@ __device__ __forceinline__ float trilerp(const float *__restrict__ m, int idx, i
 struct Gather {
     float fx, fy, fz, pterm;
     bool inb;
-    float4 t[2];   /* type-map yz-bricks at x and x+1 */
+    float4 t[2];   /* type-map yz corners at x and x+1 */
     float4 e[2];   /* elec yz-bricks */
     float4 d[2];   /* desolv yz-bricks */
 };
@@ -335,6 +336,9 @@ __device__ __forceinline__ void cell_of(const GridView &G, float x, float y, flo
     idx = (ix * G.ny + iy) * G.nz + iz;
 }
 
+#ifndef VD_TYPE_ZPAIR
+#define VD_TYPE_ZPAIR 1
+#endif
 __device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
 {
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -343,12 +347,31 @@ __device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
         : "l"(p));
 }
 
+/* packed type map m (z-pairs are 8 B/node: offset in float2 units, mstride may be odd) */
+__device__ __forceinline__ const float4 *type_map(const GridView &G, int m)
+{
+#if VD_TYPE_ZPAIR
+    return reinterpret_cast<const float4 *>(reinterpret_cast<const float2 *>(G.yz) + G.mstride * m);
+#else
+    return G.yz + G.mstride * m;
+#endif
+}
+
 __device__ __forceinline__ void issue_packed(const GridView &G, const float4 *__restrict__ ty,
                                              int idx, Gather &g)
 {
     const int nyz = G.ny * G.nz;
+#if VD_TYPE_ZPAIR
+    /* type map as z-pairs (8 B/node; 4 LDG.64): half the L2 footprint of yz-bricks */
+    const float2 *tz = reinterpret_cast<const float2 *>(ty);
+    const float2 a = __ldg(tz + idx), b = __ldg(tz + idx + G.nz);
+    const float2 c = __ldg(tz + idx + nyz), d = __ldg(tz + idx + nyz + G.nz);
+    g.t[0] = make_float4(a.x, a.y, b.x, b.y);
+    g.t[1] = make_float4(c.x, c.y, d.x, d.y);
+#else
     g.t[0] = __ldg(ty + idx);
     g.t[1] = __ldg(ty + idx + nyz);
+#endif
     ld256(G.ed + 2 * (int64_t)idx, g.e[0], g.d[0]);
     ld256(G.ed + 2 * (int64_t)(idx + nyz), g.e[1], g.d[1]);
 }
@@ -414,7 +437,7 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
         Gather c0, c1;
         {
             const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
-            const float4 *tz = G.yz + G.mstride * __float_as_int(L.atom2[i].y);
+            const float4 *tz = type_map(G, __float_as_int(L.atom2[i].y));
             int idx0, idx1;
             cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0);
             cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1);
@@ -426,7 +449,7 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
             Gather n0, n1;
             if (in < n) {
                 const float2 x = VD_S2(in, 0), y = VD_S2(in, 1), z = VD_S2(in, 2);
-                const float4 *tz = G.yz + G.mstride * __float_as_int(L.atom2[in].y);
+                const float4 *tz = type_map(G, __float_as_int(L.atom2[in].y));
                 int idx0, idx1;
                 cell_of(G, x.x, y.x, z.x, L.penalty, n0, idx0);
                 cell_of(G, x.y, y.y, z.y, L.penalty, n1, idx1);

@@ -16,7 +16,8 @@ struct vd_grid {
     int n_maps, nx, ny, nz;
     float lo[3], hi[3], spacing;
     float *d_maps;           /* (n_maps, nx, ny, nz) */
-    float4 *d_yz;            /* packed yz-bricks of every map, or null (see GridView) */
+    float4 *d_yz;            /* packed yz-bricks of the type maps, or null (see GridView) */
+    std::vector<char> yz_packed;
     std::mutex ed_lock;
     std::map<std::pair<int, int>, float4 *> d_ed;  /* packed (elec, desolv) per map pair */
 };
