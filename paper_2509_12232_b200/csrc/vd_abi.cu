@@ -186,9 +186,8 @@ vd::LigView vd_ligands::view(int l) const
     v.pij = d_pij + p0;
     v.pcoef = d_pcoef + p0;
     v.fcoef = d_fcoef + p0;
-    v.fj = d_fj + p0;
-    v.frow = d_frow + frow_start[l];
-    v.ftile = d_ftile + ftile_start[l];
+    v.fij = d_fij + p0;
+    v.n_nohb = n_nohb[l];
     v.tors = d_tors + t0;
     v.frag = d_frag;
     v.tors32 = tors32[l];
@@ -362,35 +361,22 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
             }
         }
     }
-    /* fast order: stable partition by the 12-10 flag, rows = runs of equal i,
-       rows cut at kTile boundaries of the ligand-local fast index */
+    /* fast order: stable partition by the 12-10 flag (one hb-uniform stream each) */
     std::vector<float4> fcoef(std::max(NP, 1));
-    std::vector<int> fj(std::max(NP, 1));
-    std::vector<int4> frow;
-    std::vector<int> ftile;
+    std::vector<int> fij(std::max(NP, 1));
     for (int l = 0; l < L; ++l) {
         const int p0 = a->pair_start[l], p1 = a->pair_start[l + 1];
-        s->frow_start.push_back((int)frow.size());
-        s->ftile_start.push_back((int)ftile.size());
         int w = p0;
-        for (int g = 0; g < 2; ++g)
+        for (int g = 0; g < 2; ++g) {
+            if (g == 1) s->n_nohb.push_back(w - p0);
             for (int k = p0; k < p1; ++k)
                 if ((a->pair_hb[k] ? 1 : 0) == g) {
                     fcoef[w] = pcoef[k];
-                    fj[w] = a->pair_j[k];
-                    const int i = a->pair_i[k], kl = w - p0;
-                    const bool new_tile = (kl % vd::kTile) == 0;
-                    if (new_tile) ftile.push_back((int)frow.size() - s->frow_start[l]);
-                    if (new_tile || frow.empty() || (int)frow.size() == s->frow_start[l] ||
-                        frow.back().x != i || frow.back().w != g)
-                        frow.push_back(make_int4(i, kl, kl + 1, g));
-                    else
-                        frow.back().z = kl + 1;
+                    fij[w] = a->pair_i[k] | (a->pair_j[k] << 16);
                     ++w;
                 }
-        ftile.push_back((int)frow.size() - s->frow_start[l]);
+        }
     }
-    if (frow.empty()) frow.push_back(make_int4(0, 0, 0, 0));
     bool ok = vdi::check(cudaMalloc(&s->d_atom, atom.size() * sizeof(float4)), "alloc atoms") &&
               vdi::check(cudaMalloc(&s->d_atom2, atom2.size() * sizeof(float2)), "alloc atoms2") &&
               vdi::check(cudaMalloc(&s->d_pij, pij.size() * sizeof(uint32_t)), "alloc pairs") &&
@@ -404,13 +390,9 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
               vdi::check(cudaMemcpy(s->d_tors, tors.data(), tors.size() * sizeof(int4), cudaMemcpyHostToDevice), "up tors") &&
               vdi::check(cudaMemcpy(s->d_frag, frag.data(), frag.size() * sizeof(int), cudaMemcpyHostToDevice), "up frag") &&
               vdi::check(cudaMalloc(&s->d_fcoef, fcoef.size() * sizeof(float4)), "alloc fcoef") &&
-              vdi::check(cudaMalloc(&s->d_fj, fj.size() * sizeof(int)), "alloc fj") &&
-              vdi::check(cudaMalloc(&s->d_frow, frow.size() * sizeof(int4)), "alloc frow") &&
-              vdi::check(cudaMalloc(&s->d_ftile, ftile.size() * sizeof(int)), "alloc ftile") &&
+              vdi::check(cudaMalloc(&s->d_fij, fij.size() * sizeof(int)), "alloc fij") &&
               vdi::check(cudaMemcpy(s->d_fcoef, fcoef.data(), fcoef.size() * sizeof(float4), cudaMemcpyHostToDevice), "up fcoef") &&
-              vdi::check(cudaMemcpy(s->d_fj, fj.data(), fj.size() * sizeof(int), cudaMemcpyHostToDevice), "up fj") &&
-              vdi::check(cudaMemcpy(s->d_frow, frow.data(), frow.size() * sizeof(int4), cudaMemcpyHostToDevice), "up frow") &&
-              vdi::check(cudaMemcpy(s->d_ftile, ftile.data(), ftile.size() * sizeof(int), cudaMemcpyHostToDevice), "up ftile");
+              vdi::check(cudaMemcpy(s->d_fij, fij.data(), fij.size() * sizeof(int), cudaMemcpyHostToDevice), "up fij");
     if (!ok) {
         vd_ligands_destroy(s);
         return -1;
@@ -435,9 +417,7 @@ int vd_ligands_destroy(vd_ligands *s)
     cudaFree(s->d_tors);
     cudaFree(s->d_frag);
     cudaFree(s->d_fcoef);
-    cudaFree(s->d_fj);
-    cudaFree(s->d_frow);
-    cudaFree(s->d_ftile);
+    cudaFree(s->d_fij);
     delete s;
     return 0;
 }

@@ -10,8 +10,9 @@
  * pose pair ("sub" lanes split atoms and pairs; barriers order the torsion
  * chain), which keeps enough warps resident when 12*N bytes per pose limit
  * how many poses fit in shared memory.  All loops are CTA-uniform: topology
- * and pair parameters are broadcast reads, pair parameters are staged in
- * shared-memory tiles of kTile pairs.
+ * and pair parameters are broadcast reads.  Pair parameters live in shared
+ * memory: the whole list, staged once per ligand, when it fits (the common
+ * case, <= kResidentPairs), else streamed in tiles of kTile pairs.
  *
  * Stage parity (reference paths under /root/reference/pkg/src/vecdock):
  *   A1 pose   scoring/simd.py:157-222   bit-exact in both modes: scalar IEEE
@@ -22,7 +23,8 @@
  *   A3 intra  scoring/simd.py:36-86     EXACT: canonical sequence, fp64 exp,
  *             lane-8 fp64 summation order; FAST: MUFU rsqrt/ex2/rcp + an FMA-pipe
  *             exp2 polynomial, f32x2
- *             math over a row-ordered pair stream, fp32 partials -> fp64
+ *             math over an hb-partitioned pair stream, fp32 partials per
+             kTile chunk -> fp64
  */
 #pragma once
 #include <cuda_runtime.h>
@@ -30,7 +32,8 @@
 
 namespace vd {
 
-constexpr int kTile = 256;  /* pairs per shared-memory tile (multiple of 8) */
+constexpr int kTile = 256;            /* pairs per streamed tile / fp32 partial (multiple of 8) */
+constexpr int kResidentPairs = 2048;  /* pair lists up to this stay resident in shared memory */
 
 struct GridView {
     const float *maps;      /* (n_maps, nx, ny, nz) */
@@ -57,11 +60,10 @@ struct LigView {
     /* reference order (EXACT): */
     const uint32_t *pij;    /* i | j << 15 | hb << 31 */
     const float4 *pcoef;    /* a, b, qq, dsl (weight-folded) */
-    /* fast order (FAST): pairs grouped by hb flag then row i, rows cut at tiles */
+    /* fast order (FAST): 12-6 pairs, then the n_pairs - n_nohb 12-10 pairs */
     const float4 *fcoef;
-    const int *fj;
-    const int4 *frow;       /* i, k0, k1, hb  (k = fast-order pair index) */
-    const int *ftile;       /* [n_tiles + 1]: first row of each tile */
+    const int *fij;         /* i | j << 16 */
+    int n_nohb;
     float tors32, cut2, penalty;
     int elec_map, desolv_map;
 };
@@ -196,7 +198,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
 {
 #define VD_X(k) X[(k) * NPP]
     float2 M00, M01, M02, M10, M11, M12, M20, M21, M22, TX, TY, TZ;
-    if (TPP > 1) __syncthreads();  /* scratch aliases tiles still read by the previous pose */
+    if (TPP > 1) __syncthreads();  /* S and the scratch may still be read for the previous poses */
     if (TPP == 1) {
         float m0[9], t0[3], m1[9], t1[3];
         rigid_of(g0, m0, t0);
@@ -556,23 +558,7 @@ __device__ __forceinline__ float2 pair_fast2(float2 dx, float2 dy, float2 dz, fl
     return t;
 }
 
-template <int NPP, int TPP, bool HB, bool CUT>
-__device__ __forceinline__ float2 row_fast(const float2 *S, int i, int kb, int ke,
-                                           const float4 *tc, const int *tj, int sub, float cut2)
-{
-    const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
-    float2 acc = f2(0.0f);
-#pragma unroll 4
-    for (int k = kb + sub; k < ke; k += TPP) {
-        const float4 c = tc[k];
-        const int j = tj[k];
-        acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(xi, VD_S2(j, 0)), fsub2(yi, VD_S2(j, 1)),
-                                            fsub2(zi, VD_S2(j, 2)), c, cut2));
-    }
-    return acc;
-}
-
-/* Flat variant: per-pair packed (i | j << 16), no row structure, deep unroll. */
+/* Pair stream [kb, ke) of this sub (stride TPP), deep unroll. */
 #ifndef VD_FLAT_UNROLL
 #define VD_FLAT_UNROLL 8
 #endif
@@ -593,20 +579,60 @@ __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, con
     return acc;
 }
 
-/* Shared-memory pair staging area (per CTA). */
+/* Shared-memory pair area (per CTA): the whole list (resident) or one tile. */
 struct PairTile {
-    float4 *coef;   /* [kTile] */
-    int *j;         /* [kTile] fast: j; exact: packed ij */
-    int4 *row;      /* [kTile] fast rows of the tile */
-    int2 *off;      /* [kTile] flat: pose-tile element offsets of i and j */
+    float4 *coef;   /* [cap] weight-folded a, b, qq, dsl */
+    int *j;         /* [cap] EXACT: packed ij | hb << 31 (reference order) */
+    int2 *off;      /* [cap] FAST: pose-tile element offsets 3*NPP*i, 3*NPP*j (aliases j) */
+    int cap;
+    bool resident;
 };
 
+/* Copy pairs [k0, k0 + cnt) of the mode's order into the tile (all CTA threads; caller syncs). */
+template <bool EXACT, int NPP>
+__device__ __forceinline__ void stage_pairs(const LigView &L, const PairTile &T, int k0, int cnt)
+{
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+        if (EXACT) {
+            T.coef[k] = __ldg(&L.pcoef[k0 + k]);
+            T.j[k] = (int)__ldg(&L.pij[k0 + k]);
+        } else {
+            T.coef[k] = __ldg(&L.fcoef[k0 + k]);
+            const int w = __ldg(&L.fij[k0 + k]);
+            T.off[k] = make_int2(3 * NPP * (w & 0xffff), 3 * NPP * (w >> 16));
+        }
+    }
+}
+
+/* A resident pair list is staged once per ligand, after stage_topology (same sync). */
+template <bool EXACT, int NPP>
+__device__ __forceinline__ void stage_resident(const LigView &L, const PairTile &T)
+{
+    if (T.resident) stage_pairs<EXACT, NPP>(L, T, 0, L.n_pairs);
+}
+
+template <int NPP>
+__device__ __forceinline__ void exact_pair(const float2 *S, const PairTile &T, int k, float cut2,
+                                           double &acc0, double &acc1)
+{
+    const uint32_t w = (uint32_t)T.j[k];
+    const float4 c = T.coef[k];
+    const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
+    const bool hb = w >> 31;
+    const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
+    const float2 xj = VD_S2(j, 0), yj = VD_S2(j, 1), zj = VD_S2(j, 2);
+    acc0 = __dadd_rn(acc0, (double)pair_exact(__fsub_rn(xi.x, xj.x), __fsub_rn(yi.x, yj.x),
+                                              __fsub_rn(zi.x, zj.x), hb, c, cut2));
+    acc1 = __dadd_rn(acc1, (double)pair_exact(__fsub_rn(xi.y, xj.y), __fsub_rn(yi.y, yj.y),
+                                              __fsub_rn(zi.y, zj.y), hb, c, cut2));
+}
+
 /* intra of both poses over this sub's share of the pairs (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP, bool FLAT = false>
+template <bool EXACT, int NPP, int TPP>
 __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const PairTile &T,
                                        int sub, double &a0, double &a1)
 {
-    const int n = L.n_pairs, B = NPP * TPP, tid = threadIdx.x;
+    const int n = L.n_pairs;
     if (n == 0) return;
     if (EXACT) {
         /* reference lane-8 order (scoring/simd.py:58-86): lane[k & 7] over the
@@ -615,42 +641,20 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
 #pragma unroll
         for (int l = 0; l < 8; ++l) l0[l] = l1[l] = 0.0;
         const int nblk8 = n & ~7;
-        for (int k0 = 0; k0 < n; k0 += kTile) {
-            const int cnt = min(kTile, n - k0);
-            __syncthreads();
-            for (int k = tid; k < cnt; k += B) {
-                T.coef[k] = __ldg(&L.pcoef[k0 + k]);
-                T.j[k] = (int)__ldg(&L.pij[k0 + k]);
+        const int step = T.resident ? n : T.cap;
+        for (int k0 = 0; k0 < n; k0 += step) {
+            const int cnt = min(step, n - k0);
+            if (!T.resident) {
+                __syncthreads();
+                stage_pairs<true, NPP>(L, T, k0, cnt);
+                __syncthreads();
             }
-            __syncthreads();
             const int cb = min(cnt, max(0, nblk8 - k0));  /* lane-blocked part of this tile */
             for (int kb = 0; kb < cb; kb += 8) {
 #pragma unroll
-                for (int l = 0; l < 8; ++l) {
-                    const uint32_t w = (uint32_t)T.j[kb + l];
-                    const float4 c = T.coef[kb + l];
-                    const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
-                    const bool hb = w >> 31;
-                    const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
-                    const float2 xj = VD_S2(j, 0), yj = VD_S2(j, 1), zj = VD_S2(j, 2);
-                    l0[l] = __dadd_rn(l0[l], (double)pair_exact(__fsub_rn(xi.x, xj.x), __fsub_rn(yi.x, yj.x),
-                                                                __fsub_rn(zi.x, zj.x), hb, c, L.cut2));
-                    l1[l] = __dadd_rn(l1[l], (double)pair_exact(__fsub_rn(xi.y, xj.y), __fsub_rn(yi.y, yj.y),
-                                                                __fsub_rn(zi.y, zj.y), hb, c, L.cut2));
-                }
+                for (int l = 0; l < 8; ++l) exact_pair<NPP>(S, T, kb + l, L.cut2, l0[l], l1[l]);
             }
-            for (int k = cb; k < cnt; ++k) {
-                const uint32_t w = (uint32_t)T.j[k];
-                const float4 c = T.coef[k];
-                const int i = w & 0x7fff, j = (w >> 15) & 0x7fff;
-                const bool hb = w >> 31;
-                const float2 xi = VD_S2(i, 0), yi = VD_S2(i, 1), zi = VD_S2(i, 2);
-                const float2 xj = VD_S2(j, 0), yj = VD_S2(j, 1), zj = VD_S2(j, 2);
-                tail0 = __dadd_rn(tail0, (double)pair_exact(__fsub_rn(xi.x, xj.x), __fsub_rn(yi.x, yj.x),
-                                                            __fsub_rn(zi.x, zj.x), hb, c, L.cut2));
-                tail1 = __dadd_rn(tail1, (double)pair_exact(__fsub_rn(xi.y, xj.y), __fsub_rn(yi.y, yj.y),
-                                                            __fsub_rn(zi.y, zj.y), hb, c, L.cut2));
-            }
+            for (int k = cb; k < cnt; ++k) exact_pair<NPP>(S, T, k, L.cut2, tail0, tail1);
         }
         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -663,47 +667,25 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
     } else {
         const bool cut = L.cut2 < INFINITY;
         double s0 = 0.0, s1 = 0.0;
-        int t = 0;
-        for (int k0 = 0; k0 < n; k0 += kTile, ++t) {
-            const int cnt = min(kTile, n - k0);
-            const int r0 = __ldg(&L.ftile[t]), r1 = __ldg(&L.ftile[t + 1]);
-            __syncthreads();
-            for (int k = tid; k < cnt; k += B) {
-                T.coef[k] = __ldg(&L.fcoef[k0 + k]);
-                T.j[k] = FLAT ? (__ldg(&L.fj[k0 + k]) << 16) : __ldg(&L.fj[k0 + k]);
-            }
-            for (int r = tid; r < r1 - r0; r += B) T.row[r] = __ldg(&L.frow[r0 + r]);
-            __syncthreads();
-            float2 part = f2(0.0f);
-            if (FLAT) {
-                /* expand rows into per-pair i (packed beside j), find the hb boundary */
-                __shared__ int s_kh;
-                if (tid == 0) s_kh = cnt;
-                for (int r = tid; r < r1 - r0; r += B) {
-                    const int4 row = T.row[r];
-                    for (int k = row.y - k0; k < row.z - k0; ++k)
-                        T.off[k] = make_int2(3 * NPP * row.x, 3 * NPP * (T.j[k] >> 16));
-                    if (row.w && (r == 0 || !T.row[r - 1].w)) s_kh = row.y - k0;
-                }
+        const int step = T.resident ? n : T.cap;
+        for (int t0 = 0; t0 < n; t0 += step) {
+            const int tcnt = min(step, n - t0);
+            if (!T.resident) {
                 __syncthreads();
-                const int kh = s_kh;
-                part = cut ? flat_fast<NPP, TPP, false, true>(S, 0, kh, T.coef, T.off, sub, L.cut2)
-                           : flat_fast<NPP, TPP, false, false>(S, 0, kh, T.coef, T.off, sub, L.cut2);
-                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, cnt, T.coef, T.off, sub, L.cut2)
-                                       : flat_fast<NPP, TPP, true, false>(S, kh, cnt, T.coef, T.off, sub, L.cut2));
-            } else
-            for (int r = 0; r < r1 - r0; ++r) {
-                const int4 row = T.row[r];
-                const int kb = row.y - k0, ke = row.z - k0;
-                float2 v;
-                if (row.w) v = cut ? row_fast<NPP, TPP, true, true>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2)
-                                   : row_fast<NPP, TPP, true, false>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2);
-                else v = cut ? row_fast<NPP, TPP, false, true>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2)
-                             : row_fast<NPP, TPP, false, false>(S, row.x, kb, ke, T.coef, T.j, sub, L.cut2);
-                part = fadd2(part, v);
+                stage_pairs<false, NPP>(L, T, t0, tcnt);
+                __syncthreads();
             }
-            s0 += (double)part.x;
-            s1 += (double)part.y;
+            /* fp32 partials per kTile chunk, flushed to fp64 */
+            for (int c0 = 0; c0 < tcnt; c0 += kTile) {
+                const int kb = c0, ke = min(tcnt, c0 + kTile);
+                const int kh = min(ke, max(kb, L.n_nohb - t0));  /* 12-6 | 12-10 boundary */
+                float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, kh, T.coef, T.off, sub, L.cut2)
+                                  : flat_fast<NPP, TPP, false, false>(S, kb, kh, T.coef, T.off, sub, L.cut2);
+                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, ke, T.coef, T.off, sub, L.cut2)
+                                       : flat_fast<NPP, TPP, true, false>(S, kh, ke, T.coef, T.off, sub, L.cut2));
+                s0 += (double)part.x;
+                s1 += (double)part.y;
+            }
         }
         a0 = s0;
         a1 = s1;
@@ -741,13 +723,16 @@ __device__ __forceinline__ void reduce_subs(double *red, int pp, int sub, double
 /* Dynamic shared-memory layout of the scoring CTAs. */
 struct SmemLayout {
     unsigned topo_atom, topo_atom2, topo_tors, topo_frag, scratch;
-    unsigned tile_coef, tile_j, tile_row, tile_off, red, extra, bytes;
+    unsigned tile_coef, tile_idx, red, extra, bytes;
+    int cap;        /* pairs the tile holds */
+    int resident;   /* 1: the whole pair list (n_pairs <= cap) is staged once per ligand */
 };
 
 __host__ __device__ inline unsigned align16(unsigned v) { return (v + 15u) & ~15u; }
 
+/* n_pairs: the largest pair list the launch serves (selects resident vs streamed). */
 __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n_frag, int npp,
-                                                  int tpp, unsigned extra, bool alias = false)
+                                                  int tpp, unsigned extra, int n_pairs)
 {
     SmemLayout s;
     unsigned off = align16(8u * 3u * (unsigned)n_atoms * (unsigned)npp);
@@ -759,27 +744,18 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     off = align16(off + 16u * (unsigned)n_tors);
     s.topo_frag = off;
     off = align16(off + 4u * (unsigned)n_frag);
-    /* pose-build scratch aliases the pair tiles (the pose is built before intra
-       stages pairs; build_pose2 syncs before its first scratch write) */
     const unsigned scratch_bytes = (tpp > 1) ? 4u * kPoseScratch * (unsigned)npp : 0u;
-    if (!alias || scratch_bytes > 44u * kTile) {
-        s.scratch = off;
-        off = align16(off + scratch_bytes);
-    } else {
-        s.scratch = off;  /* == tile_coef below */
-    }
+    s.scratch = off;
+    off = align16(off + scratch_bytes);
+    s.resident = n_pairs <= kResidentPairs;
+    s.cap = s.resident ? (((n_pairs > 0 ? n_pairs : 1) + 7) & ~7) : kTile;
     s.tile_coef = off;
-    off += 16u * kTile;
-    s.tile_row = off;
-    off += 16u * kTile;
-    s.tile_j = off;
-    off += 4u * kTile;
-    off = align16(off);
-    s.tile_off = off;
-    off += 8u * kTile;
-    /* sub reduction reuses the pair tiles (intra is finished when it runs) */
+    off += 16u * (unsigned)s.cap;
+    s.tile_idx = off;
+    off = align16(off + 8u * (unsigned)s.cap);
+    /* the sub reduction reuses a streamed tile (intra is finished when it runs) */
     const unsigned red_bytes = (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
-    if (red_bytes <= 44u * kTile) {
+    if (!s.resident && red_bytes <= 24u * (unsigned)s.cap) {
         s.red = s.tile_coef;
     } else {
         s.red = off;
@@ -788,6 +764,17 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     s.extra = align16(off);
     s.bytes = align16(s.extra + extra);
     return s;
+}
+
+__device__ __forceinline__ PairTile pair_tile(unsigned char *smem, const SmemLayout &lay)
+{
+    PairTile T;
+    T.coef = reinterpret_cast<float4 *>(smem + lay.tile_coef);
+    T.j = reinterpret_cast<int *>(smem + lay.tile_idx);
+    T.off = reinterpret_cast<int2 *>(smem + lay.tile_idx);
+    T.cap = lay.cap;
+    T.resident = lay.resident;
+    return T;
 }
 
 }  // namespace vd

@@ -154,10 +154,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
     extern __shared__ __align__(16) unsigned char smem[];
     const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
-    PairTile Tl{reinterpret_cast<float4 *>(smem + lay.base.tile_coef),
-                reinterpret_cast<int *>(smem + lay.base.tile_j),
-                reinterpret_cast<int4 *>(smem + lay.base.tile_row),
-                reinterpret_cast<int2 *>(smem + lay.base.tile_off)};
+    const PairTile Tl = pair_tile(smem, lay.base);
     double *red = reinterpret_cast<double *>(smem + lay.base.red);
     float *fit = reinterpret_cast<float *>(smem + lay.off_fit);
     double *e64 = reinterpret_cast<double *>(smem + lay.off_e);
@@ -178,6 +175,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
         const int l = order ? order[slot] : slot;
         const LigView L = stage_topology(ligs[l], smem, lay.base.topo_atom, lay.base.topo_atom2,
                                          lay.base.topo_tors, lay.base.topo_frag);
+        stage_resident<EXACT, NPP>(L, Tl);
         const int T = L.n_torsions, G = 7 + T;
         const uint64_t k0 = seed, k1 = (uint64_t)(base + l);
         double *cur = buf0, *nxt = buf1;
@@ -193,7 +191,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 inter2<EXACT, NPP, TPP>(L, Gv, S, sub, e0, e1);
-                intra2<EXACT, NPP, TPP, !EXACT>(L, S, Tl, sub, a0, a1);
+                intra2<EXACT, NPP, TPP>(L, S, Tl, sub, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
@@ -364,15 +362,16 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             return (int64_t)views[x].n_pairs + 4 * views[x].n_atoms >
                    (int64_t)views[y].n_pairs + 4 * views[y].n_atoms;
         });
-        int nmax = 1, tb = 0, fb = 0;
+        int nmax = 1, tb = 0, fb = 0, pmax = 0;
         for (int l : v) {
             nmax = std::max(nmax, views[l].n_atoms);
             tb = std::max(tb, views[l].n_torsions);
             fb = std::max(fb, views[l].n_frag);
+            pmax = std::max(pmax, views[l].n_pairs);
         }
         Launch L;
         int npp0;
-        if (vd::pick_shape(nmax, exact, &npp0, &L.tpp)) return -1;
+        if (vd::pick_shape(nmax, pmax, exact, &npp0, &L.tpp)) return -1;
         /* pose-pairs per CTA: the candidate with most resident warps per SM
            (VD_GA_NPP forces one, for tuning) */
         int best_warps = -1;
@@ -380,7 +379,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         for (int npp : {32, 64, 16}) {  /* ties -> 32 (cfg2 A/B: 6078 vs 5837 ligands/s) */
             if (force && atoi(force) != npp) continue;
             vd::GaLayout lay;
-            lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra);
+            lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra, pmax);
             if (lay.base.bytes > 227u * 1024u) continue;
             int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes) * npp * L.tpp / 32;
             if (npp == 64) warps -= 4;  /* measured: 64 needs clearly more warps to win */

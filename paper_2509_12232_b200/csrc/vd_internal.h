@@ -35,11 +35,9 @@ struct vd_ligands {
     float4 *d_pcoef;
     int4 *d_tors;
     int *d_frag;
-    float4 *d_fcoef;          /* fast-order pairs */
-    int *d_fj;
-    int4 *d_frow;
-    int *d_ftile;
-    std::vector<int> frow_start, ftile_start, n_frag;  /* per-ligand offsets into d_frow / d_ftile */
+    float4 *d_fcoef;          /* fast-order pairs: 12-6 then 12-10 */
+    int *d_fij;               /* i | j << 16 */
+    std::vector<int> n_nohb, n_frag;
     vd::LigView view(int lig) const;
 };
 
@@ -54,7 +52,7 @@ bool make_packed(vd_grid *g);
 }  // namespace vdi
 
 namespace vd {
-int pick_shape(int n_atoms, bool exact, int *npp, int *tpp);
+int pick_shape(int n_atoms, int n_pairs, bool exact, int *npp, int *tpp);
 }
 
 #define VD_CK(call)                                        \

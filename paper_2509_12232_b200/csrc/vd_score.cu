@@ -14,7 +14,7 @@
 
 namespace vd {
 
-template <bool EXACT, int NPP, int TPP, bool FLAT>
+template <bool EXACT, int NPP, int TPP>
 __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
                                                          const double *__restrict__ genes,
                                                          const float *__restrict__ poses,
@@ -26,12 +26,10 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     extern __shared__ __align__(16) unsigned char smem[];
     const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
-    PairTile T{reinterpret_cast<float4 *>(smem + lay.tile_coef),
-               reinterpret_cast<int *>(smem + lay.tile_j),
-               reinterpret_cast<int4 *>(smem + lay.tile_row),
-               reinterpret_cast<int2 *>(smem + lay.tile_off)};
+    const PairTile T = pair_tile(smem, lay);
     const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
                                      lay.topo_frag);
+    stage_resident<EXACT, NPP>(L, T);
     __syncthreads();
     const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
     const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;  /* tail: duplicate, drop */
@@ -48,7 +46,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
     inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
-    intra2<EXACT, NPP, TPP, FLAT>(L, S, T, sub, a0, a1);
+    intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
@@ -89,7 +87,7 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
 }
 
 /* Launch shape for a ligand: pose pairs per CTA (NPP) and threads per pair (TPP). */
-int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
+int pick_shape(int n_atoms, int n_pairs, bool exact, int *npp, int *tpp)
 {
     const unsigned limit = 200 * 1024;
     /* threads per pose pair: more subs for larger ligands, where 12*N bytes of
@@ -108,7 +106,7 @@ int pick_shape(int n_atoms, bool exact, int *npp, int *tpp)
     const int pref_fast[3] = {32, 16, 64}, pref_exact[3] = {64, 32, 16};
     for (int n : (exact ? pref_exact : pref_fast)) {
         if (force_npp && n != force_npp) continue;
-        if (smem_layout(n_atoms, 64, 4 * n_atoms, n, t, 0).bytes <= limit) {
+        if (smem_layout(n_atoms, 64, 4 * n_atoms, n, t, 0, n_pairs).bytes <= limit) {
             *npp = n;
             *tpp = t;
             return 0;
@@ -124,12 +122,8 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
                             const float *poses, int64_t P, int ngenes, double *inter,
                             double *intra, float *total, cudaStream_t st)
 {
-    /* aliasing the pose scratch into the pair tiles buys a third CTA per SM at
-       TPP=2 but measured 24% slower on B200 (2.98 vs 2.40 ms, cfg1); opt-in only */
-    static const bool alias = getenv("VD_ALIAS") != nullptr;
-    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0, alias);
-    static const bool flat = getenv("VD_ROWS") == nullptr;  /* flat pair stream (A/B: VD_ROWS=1) */
-    auto k = flat ? score_kernel<EXACT, NPP, TPP, true> : score_kernel<EXACT, NPP, TPP, false>;
+    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0, L.n_pairs);
+    auto k = score_kernel<EXACT, NPP, TPP>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
     if (e != cudaSuccess) return e;
     const int64_t per_cta = 2 * NPP;
@@ -146,7 +140,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
 {
     const bool exact = mode == VD_MODE_EXACT;
     int npp, tpp;
-    if (pick_shape(L.n_atoms, exact, &npp, &tpp)) return cudaErrorInvalidValue;
+    if (pick_shape(L.n_atoms, L.n_pairs, exact, &npp, &tpp)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
     const double *g = src == 0 ? genes : nullptr;
     const float *p = src == 0 ? nullptr : poses;
@@ -165,9 +159,9 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
                         cudaStream_t st)
 {
     int npp, tpp;
-    if (pick_shape(L.n_atoms, true, &npp, &tpp)) return cudaErrorInvalidValue;
+    if (pick_shape(L.n_atoms, 0, true, &npp, &tpp)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
-    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, 1, 0);
+    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, 1, 0, 0);
     const size_t smem = lay.bytes;
     const int64_t blocks = (P + 2 * npp - 1) / (2 * npp);
     cudaError_t e;
