@@ -18,6 +18,8 @@ from .context import BackendUnavailable
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libvdb200.so"
+if os.environ.get("VD_LIB"):  # A/B tuning only: a variant build of the same library
+    LIB_PATH = Path(os.environ["VD_LIB"]).resolve()
 
 MODE_FAST = 0
 MODE_EXACT = 1

@@ -18,8 +18,12 @@
 
 #include "vd_internal.h"
 
-#ifndef VD_TYPE_ZPAIR
-#define VD_TYPE_ZPAIR 1
+/* L2 share a packed copy may touch: B200's 126 MB L2 is split over two dies and lines
+ * read from both dies are cached on both, so a map set gathered by every SM thrashes
+ * well below 126 MB (cfg1: the 74 MB yz-brick copy read 1.19 GB of DRAM per 1M-pose
+ * launch; the 45 MB z-pair copy 166 MB) */
+#ifndef VD_BRICK_BUDGET_MB
+#define VD_BRICK_BUDGET_MB 48
 #endif
 
 namespace vd {
@@ -87,19 +91,22 @@ __global__ void pack_ed(const float *__restrict__ e, const float *__restrict__ d
     }
 }
 
-/* Build the packed gather copy when it stays comfortably L2-resident (126 MB L2). */
+/* Build the packed gather copy when it stays L2-resident.  Type maps are yz-bricks (2
+ * LDG.128 per atom) when the touched copy -- every type map plus the 32-B elec/desolv
+ * bricks -- fits the budget above, else z-pairs (4 LDG.64 per atom, half the footprint;
+ * cfg2's 64^3 grid takes bricks, cfg1's 80^3 z-pairs), else nothing (plain gathers). */
 bool make_packed(vd_grid *g)
 {
     const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
-    const int64_t bytes = nodes * ((VD_TYPE_ZPAIR ? 8 : 16) * (int64_t)g->n_maps + 32);
-    if (getenv("VD_NO_PACK") || bytes > (int64_t)96 << 20) return true;
+    const int64_t n_type = g->n_maps > 2 ? g->n_maps - 2 : 1;
+    const int64_t brick = nodes * (16 * n_type + 32), zpair = nodes * (8 * n_type + 32);
+    if (getenv("VD_NO_PACK") || zpair > (int64_t)96 << 20) return true;
+    const char *ov = getenv("VD_BRICK_BUDGET_MB");  /* tests force either layout */
+    g->zpair = brick > ((ov ? atoll(ov) : (int64_t)VD_BRICK_BUDGET_MB) << 20);
     /* type maps are packed lazily in ed_for(): only the maps a ligand set can
-       reference (every map except its elec/desolv pair).  Type maps use z-pairs
-       (8 B/node), not yz-bricks (16 B/node): at cfg1 the brick copy (74 MB touched)
-       thrashed L2 (834 MB DRAM read per 1M-pose launch vs 168 MB with z-pairs,
-       and 1.7% slower) - profiles/r1_score_kernel.md */
+       reference (every map except its elec/desolv pair) */
     g->yz_packed.assign(g->n_maps, 0);
-    return check(cudaMalloc(&g->d_yz, (VD_TYPE_ZPAIR ? sizeof(float2) : sizeof(float4)) * nodes * g->n_maps), "alloc yz");
+    return check(cudaMalloc(&g->d_yz, (g->zpair ? sizeof(float2) : sizeof(float4)) * nodes * g->n_maps), "alloc yz");
 }
 
 static const float4 *ed_for(const vd_grid *gc, int e, int d)
@@ -118,12 +125,11 @@ static const float4 *ed_for(const vd_grid *gc, int e, int d)
     pack_ed<<<1184, 256>>>(g->d_maps + nodes * e, g->d_maps + nodes * d, nodes, g->ny, g->nz, p);
     for (int m = 0; m < g->n_maps; ++m)
         if (m != e && m != d && !g->yz_packed[m]) {
-#if VD_TYPE_ZPAIR
-            pack_z<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->nz,
-                                  reinterpret_cast<float2 *>(g->d_yz) + nodes * m);
-#else
-            pack_yz<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->ny, g->nz, g->d_yz + nodes * m);
-#endif
+            if (g->zpair)
+                pack_z<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->nz,
+                                      reinterpret_cast<float2 *>(g->d_yz) + nodes * m);
+            else
+                pack_yz<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->ny, g->nz, g->d_yz + nodes * m);
             g->yz_packed[m] = 1;
         }
     if (cudaDeviceSynchronize() != cudaSuccess) {
@@ -148,6 +154,8 @@ vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)
     v.lo0 = g->lo[0]; v.lo1 = g->lo[1]; v.lo2 = g->lo[2];
     v.hi0 = g->hi[0]; v.hi1 = g->hi[1]; v.hi2 = g->hi[2];
     v.spacing = g->spacing;
+    v.one = 1.0f;
+    v.zpair = g->zpair ? 1 : 0;
     return v;
 }
 

@@ -41,14 +41,17 @@ struct GridView {
     int64_t mstride;        /* nx * ny * nz */
     float lo0, lo1, lo2, hi0, hi1, hi2, spacing;
     /* packed gather layout (null when the packed copy would not stay L2-resident):
-     *   yz[m][node]  = (v[z], v[z+1])  z-pair, 8 B (VD_TYPE_ZPAIR=1, default), or the
-     *                  yz-brick (v[y,z], v[y,z+1], v[y+1,z], v[y+1,z+1]), 16 B (=0)
+     *   yz[m][node]  = the yz-brick (v[y,z], v[y,z+1], v[y+1,z], v[y+1,z+1]), 16 B, when
+     *                  the touched copy fits the L2 share (zpair = 0), else the z-pair
+     *                  (v[z], v[z+1]), 8 B (zpair = 1)
      *   ed[2*node]   = elec yz-brick, ed[2*node+1] = desolv yz-brick (32 B, one LDG.256)
-     * -> 4 LDG.64 + 2 LDG.256 per atom instead of 24 scalar gathers: each
-     *    scattered warp-wide load costs ~one L1TEX wavefront per lane, so the
+     * -> 2 LDG.128 (or 4 LDG.64) + 2 LDG.256 per atom instead of 24 scalar gathers:
+     *    each scattered warp-wide load costs ~one L1TEX wavefront per lane, so the
      *    gather cost scales with load instructions, not bytes */
     const float4 *yz;
     const float4 *ed;
+    int zpair;
+    float one;              /* 1.0f, opaque to ptxas: fma(p, one, q) is an uncontractible p + q */
 };
 
 struct LigView {
@@ -338,9 +341,6 @@ __device__ __forceinline__ void cell_of(const GridView &G, float x, float y, flo
     idx = (ix * G.ny + iy) * G.nz + iz;
 }
 
-#ifndef VD_TYPE_ZPAIR
-#define VD_TYPE_ZPAIR 1
-#endif
 __device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
 {
     asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -349,31 +349,28 @@ __device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
         : "l"(p));
 }
 
-/* packed type map m (z-pairs are 8 B/node: offset in float2 units, mstride may be odd) */
+/* packed type map m: z-pairs are 8 B/node (offset in float2 units), yz-bricks 16 B */
 __device__ __forceinline__ const float4 *type_map(const GridView &G, int m)
 {
-#if VD_TYPE_ZPAIR
-    return reinterpret_cast<const float4 *>(reinterpret_cast<const float2 *>(G.yz) + G.mstride * m);
-#else
-    return G.yz + G.mstride * m;
-#endif
+    return G.zpair ? reinterpret_cast<const float4 *>(reinterpret_cast<const float2 *>(G.yz) + G.mstride * m)
+                   : G.yz + G.mstride * m;
 }
 
 __device__ __forceinline__ void issue_packed(const GridView &G, const float4 *__restrict__ ty,
                                              int idx, Gather &g)
 {
     const int nyz = G.ny * G.nz;
-#if VD_TYPE_ZPAIR
-    /* type map as z-pairs (8 B/node; 4 LDG.64): half the L2 footprint of yz-bricks */
-    const float2 *tz = reinterpret_cast<const float2 *>(ty);
-    const float2 a = __ldg(tz + idx), b = __ldg(tz + idx + G.nz);
-    const float2 c = __ldg(tz + idx + nyz), d = __ldg(tz + idx + nyz + G.nz);
-    g.t[0] = make_float4(a.x, a.y, b.x, b.y);
-    g.t[1] = make_float4(c.x, c.y, d.x, d.y);
-#else
-    g.t[0] = __ldg(ty + idx);
-    g.t[1] = __ldg(ty + idx + nyz);
-#endif
+    if (G.zpair) {
+        /* type map as z-pairs (8 B/node; 4 LDG.64): half the L2 footprint of yz-bricks */
+        const float2 *tz = reinterpret_cast<const float2 *>(ty);
+        const float2 a = __ldg(tz + idx), b = __ldg(tz + idx + G.nz);
+        const float2 c = __ldg(tz + idx + nyz), d = __ldg(tz + idx + nyz + G.nz);
+        g.t[0] = make_float4(a.x, a.y, b.x, b.y);
+        g.t[1] = make_float4(c.x, c.y, d.x, d.y);
+    } else {
+        g.t[0] = __ldg(ty + idx);
+        g.t[1] = __ldg(ty + idx + nyz);
+    }
     ld256(G.ed + 2 * (int64_t)idx, g.e[0], g.d[0]);
     ld256(G.ed + 2 * (int64_t)(idx + nyz), g.e[1], g.d[1]);
 }
@@ -397,11 +394,44 @@ __device__ __forceinline__ float tri_b(const float4 &b0, const float4 &b1, float
     return tri8(b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, fx, fy, fz);
 }
 
-__device__ __forceinline__ float finish_packed(const Gather &g, float q, float dsf)
+#ifndef VD_PACKED_LERP
+#define VD_PACKED_LERP 1
+#endif
+/* Two reference lerps at once in f32x2: (a*(1-t)) + (b*t) with both products rounded and
+ * the sum written as fma(p, one, q) -- ptxas contracts packed mul + add into FFMA2 (see
+ * mul2 above) but cannot fold a product into an fma whose multiplier it does not know. */
+__device__ __forceinline__ float2 plerp(float2 a, float2 b, float2 omt, float2 t, float2 one)
 {
+    return __ffma2_rn(__fmul2_rn(a, omt), one, __fmul2_rn(b, t));
+}
+
+/* tri_b with the x- and y-collapses paired: (c00, c01) and (c10, c11) are lerps of the
+ * z-adjacent corner pairs, then (c0, c1) one more packed lerp; the z-lerp is scalar.
+ * Same operations and rounding as tri8. */
+__device__ __forceinline__ float tri_bp(const float4 &b0, const float4 &b1, float2 X, float2 OX,
+                                        float2 Y, float2 OY, float fz, float omz, float2 one)
+{
+    const float2 cz0 = plerp(f2(b0.x, b0.y), f2(b1.x, b1.y), OX, X, one);
+    const float2 cz1 = plerp(f2(b0.z, b0.w), f2(b1.z, b1.w), OX, X, one);
+    const float2 c = plerp(cz0, cz1, OY, Y, one);
+    return __fadd_rn(__fmul_rn(c.x, omz), __fmul_rn(c.y, fz));
+}
+
+__device__ __forceinline__ float finish_packed(const Gather &g, float q, float dsf, float one)
+{
+#if VD_PACKED_LERP
+    const float2 ONE = f2(one);
+    const float2 X = f2(g.fx), OX = f2(__fsub_rn(1.0f, g.fx));
+    const float2 Y = f2(g.fy), OY = f2(__fsub_rn(1.0f, g.fy));
+    const float omz = __fsub_rn(1.0f, g.fz);
+    const float vt = tri_bp(g.t[0], g.t[1], X, OX, Y, OY, g.fz, omz, ONE);
+    const float ve = tri_bp(g.e[0], g.e[1], X, OX, Y, OY, g.fz, omz, ONE);
+    const float vd = tri_bp(g.d[0], g.d[1], X, OX, Y, OY, g.fz, omz, ONE);
+#else
     const float vt = tri_b(g.t[0], g.t[1], g.fx, g.fy, g.fz);
     const float ve = tri_b(g.e[0], g.e[1], g.fx, g.fy, g.fz);
     const float vd = tri_b(g.d[0], g.d[1], g.fx, g.fy, g.fz);
+#endif
     const float gterm = __fadd_rn(__fadd_rn(vt, __fmul_rn(q, ve)), __fmul_rn(dsf, vd));
     return g.inb ? gterm : g.pterm;
 }
@@ -459,8 +489,8 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
                 issue_packed(G, tz, idx1, n1);
             }
             const float q = L.atom[i].w, dsf = L.atom2[i].x;
-            e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf));
-            e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf));
+            e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
+            e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
             c0 = n0;
             c1 = n1;
         }
@@ -690,6 +720,69 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
         a0 = s0;
         a1 = s1;
     }
+}
+
+/* FAST inter + intra interleaved (packed maps, resident pair list): the grid gathers of
+ * one atom are issued, then a slice of the pair stream runs while they are in flight, then
+ * the atom is interpolated.  The slices are CTA-uniform ranges of the flat pair stream
+ * (each split at the 12-6 | 12-10 boundary), so every pair is still visited by exactly
+ * one sub of the pose pair with broadcast parameter loads, and no barrier is needed. */
+#ifndef VD_FUSED
+#define VD_FUSED 0
+#endif
+template <int NPP, int TPP>
+__device__ __forceinline__ void fused_fast(const LigView &L, const GridView &G, const float2 *S,
+                                           const PairTile &T, int sub, double &e0, double &e1,
+                                           double &a0, double &a1)
+{
+    const int n = L.n_atoms, np = L.n_pairs, kh = L.n_nohb;
+    const bool cut = L.cut2 < INFINITY;
+    const int nit = (n + TPP - 1) / TPP;  /* CTA-uniform atom iterations */
+    Gather c0, c1;
+    auto issue = [&](int i) {
+        const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
+        const float4 *tz = type_map(G, __float_as_int(L.atom2[i].y));
+        int idx0, idx1;
+        cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0);
+        cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1);
+        issue_packed(G, tz, idx0, c0);
+        issue_packed(G, tz, idx1, c1);
+    };
+    if (sub < n) issue(sub);
+    double s0 = 0.0, s1 = 0.0;
+    for (int it = 0; it < nit; ++it) {
+        const int kb = (int)((int64_t)np * it / nit), ke = (int)((int64_t)np * (it + 1) / nit);
+        const int km = min(ke, max(kb, kh));
+        float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, km, T.coef, T.off, sub, L.cut2)
+                          : flat_fast<NPP, TPP, false, false>(S, kb, km, T.coef, T.off, sub, L.cut2);
+        part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, km, ke, T.coef, T.off, sub, L.cut2)
+                               : flat_fast<NPP, TPP, true, false>(S, km, ke, T.coef, T.off, sub, L.cut2));
+        s0 += (double)part.x;
+        s1 += (double)part.y;
+        const int i = sub + it * TPP;
+        if (i < n) {
+            const float q = L.atom[i].w, dsf = L.atom2[i].x;
+            e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
+            e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
+            if (i + TPP < n) issue(i + TPP);
+        }
+    }
+    a0 = s0;
+    a1 = s1;
+}
+
+/* inter + intra of both poses (all CTA threads must call) */
+template <bool EXACT, int NPP, int TPP>
+__device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
+                                        const PairTile &T, int sub, double &e0, double &e1,
+                                        double &a0, double &a1)
+{
+    if (VD_FUSED && !EXACT && G.yz != nullptr && T.resident) {
+        fused_fast<NPP, TPP>(L, G, S, T, sub, e0, e1, a0, a1);
+        return;
+    }
+    inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
+    intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }
 
 __device__ __forceinline__ float total32(double inter, double intra, float tors)

@@ -82,8 +82,9 @@ __device__ __forceinline__ double dquat_norm(const double *q)
 __device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0, uint64_t k1, double *g)
 {
     const double PI = 3.141592653589793;
+    vd_words W = vd_words_at(i, 0, VD_PH_INIT_U, k0, k1);
     for (int a = 0; a < 3; ++a) {
-        const double u = vd_u01(vd_word(a, i, 0, VD_PH_INIT_U, k0, k1));
+        const double u = vd_u01(vd_words_get(&W, a));
         g[a] = __dadd_rn(P.lo[a], __dmul_rn(__dsub_rn(P.hi[a], P.lo[a]), u));
     }
     double q[4];
@@ -92,7 +93,7 @@ __device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0, uint6
     if (n < 1e-12) { q[0] = 1.0; q[1] = q[2] = q[3] = 0.0; n = 1.0; }
     for (int c = 0; c < 4; ++c) g[3 + c] = __ddiv_rn(q[c], n);
     for (int t = 0; t < T; ++t) {
-        const double u = vd_u01(vd_word(4 + t, i, 0, VD_PH_INIT_U, k0, k1));
+        const double u = vd_u01(vd_words_get(&W, 4 + t));
         g[7 + t] = __dadd_rn(-PI, __dmul_rn(2.0 * PI, u));
     }
 }
@@ -101,32 +102,43 @@ __device__ void breed_child(const GaDev &P, int G, const double *cur, const floa
                             int c, uint64_t k0, uint64_t k1, double *child)
 {
     const int k = P.tournament;
+    vd_words W = vd_words_at(c, gen, VD_PH_BREED_U, k0, k1);  /* one Philox block per 4 slots */
     int win[2];
     for (int r = 0; r < 2; ++r) {
         int best = -1;
         for (int j = 0; j < k; ++j) {
-            const int idx = (int)vd_below(vd_word(r * k + j, c, gen, VD_PH_BREED_U, k0, k1),
+            const int idx = (int)vd_below(vd_words_get(&W, r * k + j),
                                           (uint64_t)P.pop);
             if (best < 0 || fit[idx] < fit[best]) best = idx;
         }
         win[r] = best;
     }
     const double *p1 = cur + (size_t)win[0] * G, *p2 = cur + (size_t)win[1] * G;
-    const bool do_cx = vd_u01(vd_word(2 * k, c, gen, VD_PH_BREED_U, k0, k1)) < P.cx_rate;
-    const int a = (int)vd_below(vd_word(2 * k + 1, c, gen, VD_PH_BREED_U, k0, k1), (uint64_t)G + 1);
-    const int b = (int)vd_below(vd_word(2 * k + 2, c, gen, VD_PH_BREED_U, k0, k1), (uint64_t)G + 1);
+    const bool do_cx = vd_u01(vd_words_get(&W, 2 * k)) < P.cx_rate;
+    const int a = (int)vd_below(vd_words_get(&W, 2 * k + 1), (uint64_t)G + 1);
+    const int b = (int)vd_below(vd_words_get(&W, 2 * k + 2), (uint64_t)G + 1);
     const int c_lo = min(a, b), c_hi = max(a, b);
     bool mut_rot = false;
-    for (int g = 0; g < G; ++g) {
-        const double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
-        const bool mut = vd_u01(vd_word(2 * k + 3 + g, c, gen, VD_PH_BREED_U, k0, k1)) < P.mut_rate;
-        double noise = 0.0;
-        if (mut) {
+    /* genes in chunks of 32: first the crossover copy (+0.0, as child + where(mut, z*sigma, 0))
+       and the mutation mask, then the normals for the set bits only, so a warp runs the
+       normal sampler max-over-lanes(mutations) times rather than once per gene with any
+       mutating lane */
+    for (int g0 = 0; g0 < G; g0 += 32) {
+        const int g1 = min(G, g0 + 32);
+        uint32_t mask = 0;
+        for (int g = g0; g < g1; ++g) {
+            const double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
+            if (vd_u01(vd_words_get(&W, 2 * k + 3 + g)) < P.mut_rate) mask |= 1u << (g - g0);
+            child[g] = __dadd_rn(v, 0.0);
+        }
+        while (mask) {
+            const int g = g0 + __ffs(mask) - 1;
+            mask &= mask - 1;
+            const double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
             const double sig = g < 3 ? P.sigma_t : (g < 7 ? P.sigma_r : P.sigma_tor);
-            noise = __dmul_rn(vd_normal(g, c, gen, VD_PH_BREED_N, k0, k1), sig);
+            child[g] = __dadd_rn(v, __dmul_rn(vd_normal(g, c, gen, VD_PH_BREED_N, k0, k1), sig));
             mut_rot |= (g >= 3 && g < 7);
         }
-        child[g] = __dadd_rn(v, noise);
     }
     double n = dquat_norm(child + 3);
     const bool bad = n < 1e-9;
@@ -143,8 +155,11 @@ struct GaLayout {
     unsigned off_fit, off_e, off_a, off_taken;
 };
 
+#ifndef VD_GA_MINB
+#define VD_GA_MINB 1
+#endif
 template <bool EXACT, int NPP, int TPP>
-__global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+__global__ void __launch_bounds__(NPP *TPP, VD_GA_MINB) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, int count,
                                                       GaDev P, uint64_t seed, int64_t base,
                                                       int *work, double *gene_buf, int gmax,
@@ -190,8 +205,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_kernel(GridView Gv, const LigView
                 build_pose2<NPP, TPP>(L, cur + (size_t)q0 * G, cur + (size_t)q1 * G, S, sub,
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                inter2<EXACT, NPP, TPP>(L, Gv, S, sub, e0, e1);
-                intra2<EXACT, NPP, TPP>(L, S, Tl, sub, a0, a1);
+                energy2<EXACT, NPP, TPP>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }

@@ -185,4 +185,29 @@ VD_HD uint64_t vd_word(uint64_t slot, uint64_t idx, uint64_t gen, uint64_t phase
     return w.v[slot & 3];
 }
 
+/* The same words as vd_word for one (idx, gen, phase), read at non-decreasing
+ * slots: each Philox block (4 slots) is generated once instead of per word. */
+typedef struct {
+    uint64_t idx, gen, phase, k0, k1, blk;
+    vd_u64x4 w;
+} vd_words;
+
+VD_HD vd_words vd_words_at(uint64_t idx, uint64_t gen, uint64_t phase, uint64_t k0, uint64_t k1)
+{
+    vd_words s;
+    s.idx = idx; s.gen = gen; s.phase = phase; s.k0 = k0; s.k1 = k1;
+    s.blk = ~(uint64_t)0;
+    s.w.v[0] = s.w.v[1] = s.w.v[2] = s.w.v[3] = 0;
+    return s;
+}
+
+VD_HD uint64_t vd_words_get(vd_words *s, uint64_t slot)
+{
+    if ((slot >> 2) != s->blk) {
+        s->blk = slot >> 2;
+        s->w = vd_philox4x64_10(s->blk, s->idx, s->gen, s->phase, s->k0, s->k1);
+    }
+    return s->w.v[slot & 3];
+}
+
 #endif /* VD_RNG_H */

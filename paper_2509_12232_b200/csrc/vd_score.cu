@@ -45,8 +45,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
         if (TPP > 1) __syncthreads();
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-    inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
-    intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
+    energy2<EXACT, NPP, TPP>(L, G, S, T, sub, e0, e1, a0, a1);
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {

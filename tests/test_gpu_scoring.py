@@ -239,22 +239,35 @@ def test_grid_builder_vs_reference(case):
         assert rel.max() < 1e-4, (label, rel.max())
 
 
-@pytest.mark.parametrize("name", ["cfg1", "big"])
-def test_fast_mode_plain_grid_layout(cuda, name, monkeypatch):
-    """The unpacked (n_maps, nx, ny, nz) gather path (used when the packed copy would
-    not stay L2-resident, e.g. cfg4's 126^3 grid) agrees like the packed one."""
+LAYOUTS = {"plain": ("VD_NO_PACK", "1"), "zpair": ("VD_BRICK_BUDGET_MB", "0"),
+           "brick": ("VD_BRICK_BUDGET_MB", "100000")}
+
+
+def _score_with_layout(c, layout, monkeypatch):
     from paper_2509_12232_b200 import gridmaps
     from paper_2509_12232_b200.backend import CudaBackend
     from paper_2509_12232_b200.context import prepare_context
 
-    monkeypatch.setenv("VD_NO_PACK", "1")
-    c = fx.pop_case(name)
+    monkeypatch.setenv(*LAYOUTS[layout])
     g2 = gridmaps.GridMapSet(c["grid"].spec, dict(c["grid"].maps))  # fresh device grid
     ctx = prepare_context(c["topo"], g2)
-    b = CudaBackend(mode="fast", device=0)
-    e, a, t = b.score_population_arrays(c["genes"], ctx)
+    return CudaBackend(mode="fast", device=0).score_population_arrays(c["genes"], ctx)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "big"])
+@pytest.mark.parametrize("layout", sorted(LAYOUTS))
+def test_fast_mode_every_grid_layout(cuda, name, layout, monkeypatch):
+    """Each gather layout -- plain (n_maps, nx, ny, nz) maps (the packed copy would not stay
+    L2-resident, e.g. cfg4's 126^3 grid), z-pair type maps (cfg1) and yz-brick type maps
+    (cfg2) -- agrees with the reference, and the inter energies are bit-identical across
+    layouts (same corner values, same lerp arithmetic, same summation order)."""
+    c = fx.pop_case(name)
+    e, a, t = _score_with_layout(c, layout, monkeypatch)
     assert fx.within_tol(t, c["total"]).all()
     assert fx.within_tol(e, c["inter"]).all()
+    monkeypatch.undo()
+    e0, _, _ = _score_with_layout(c, "plain", monkeypatch)
+    assert np.array_equal(e.view(np.uint64), e0.view(np.uint64))
 
 
 @pytest.mark.parametrize("tpp", ["1", "2", "4", "8"])

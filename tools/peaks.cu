@@ -2,6 +2,10 @@
 // carries only HBM copy and bf16 GEMM figures):
 //   vdp_fp32_peak:  packed FFMA2 throughput (8 independent chains per thread)
 //   vdp_l2_gather:  random 8-byte gathers from an L2-resident buffer
+//   vdp_atom_gather: the score kernel's own per-atom gather pattern -- 4 LDG.64
+//                    z-pair corners of a random type map + 2 LDG.256 elec/desolv
+//                    bricks (96 B per atom) at uniformly random cells of
+//                    same-size packed maps; the ceiling of the inter stage
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,6 +39,40 @@ __global__ void gather_kernel(const float2 *__restrict__ buf, uint64_t mask, int
         for (int k = 0; k < 8; ++k) acc = __fadd2_rn(acc, v[k]);
     }
     if (acc.x == 12345.0f) out[0] = acc;
+}
+
+__device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
+{
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z),
+                   "=f"(hi.w)
+                 : "l"(p));
+}
+
+__global__ void atom_gather_kernel(const float2 *__restrict__ zp, const float4 *__restrict__ ed,
+                                   int n, int n_types, int iters, float *out)
+{
+    uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + 12345u;
+    const int nyz = n * n;
+    const int64_t mstride = (int64_t)n * nyz;
+    float acc = 0.f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll 4
+        for (int k = 0; k < 4; ++k) {
+            h ^= h << 13; h ^= h >> 17; h ^= h << 5;
+            const int ix = (h >> 4) % (n - 1), iy = (h >> 12) % (n - 1), iz = (h >> 20) % (n - 1);
+            const int m = h % n_types;
+            const int idx = (ix * n + iy) * n + iz;
+            const float2 *t = zp + mstride * m;
+            const float2 a = __ldg(t + idx), b = __ldg(t + idx + n);
+            const float2 c = __ldg(t + idx + nyz), d = __ldg(t + idx + nyz + n);
+            float4 e0, d0, e1, d1;
+            ld256(ed + 2 * (int64_t)idx, e0, d0);
+            ld256(ed + 2 * (int64_t)(idx + nyz), e1, d1);
+            acc += a.x + b.y + c.x + d.y + e0.x + d0.w + e1.y + d1.z;
+        }
+    }
+    if (acc == 12345.0f) out[0] = acc;
 }
 
 static float time_it(void (*launch)(void *), void *arg)
@@ -102,4 +140,38 @@ extern "C" double vdp_l2_gather_gbs(int64_t bytes)
     cudaFree(g.out);
     const double useful = (double)g.blocks * g.threads * g.iters * 8 * 8;  // bytes delivered
     return useful / (ms * 1e-3) / 1e9;
+}
+
+struct AArgs { const float2 *zp; const float4 *ed; int n, n_types, iters, blocks, threads; float *out; };
+static void launch_atom(void *p)
+{
+    AArgs *a = (AArgs *)p;
+    atom_gather_kernel<<<a->blocks, a->threads>>>(a->zp, a->ed, a->n, a->n_types, a->iters, a->out);
+}
+
+/* GB/s of 96-B atom gathers (the score kernel's inter pattern) over an n^3 grid
+ * with n_types z-pair type maps plus one elec/desolv brick map. */
+extern "C" double vdp_atom_gather_gbs(int n, int n_types)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t nodes = (size_t)n * n * n;
+    AArgs a;
+    cudaMalloc((void **)&a.zp, nodes * n_types * sizeof(float2));
+    cudaMalloc((void **)&a.ed, nodes * 2 * sizeof(float4));
+    cudaMemset((void *)a.zp, 0, nodes * n_types * sizeof(float2));
+    cudaMemset((void *)a.ed, 0, nodes * 2 * sizeof(float4));
+    cudaMalloc(&a.out, sizeof(float));
+    a.n = n;
+    a.n_types = n_types;
+    a.blocks = sms * 16;
+    a.threads = 128;
+    a.iters = 128;
+    const float ms = time_it(launch_atom, &a);
+    cudaFree((void *)a.zp);
+    cudaFree((void *)a.ed);
+    cudaFree(a.out);
+    const double atoms = (double)a.blocks * a.threads * a.iters * 4;
+    return atoms * 96.0 / (ms * 1e-3) / 1e9;
 }
