@@ -186,14 +186,20 @@ __device__ __forceinline__ void torsion_axis(float2 ax, float2 ay, float2 az, fl
     kz = f2(k[0][2], k[1][2]);
 }
 
-/* Scratch floats per pose pair (TPP > 1): rigid m/t of both poses (24) and the
- * current torsion's axis k and cos/sin for both poses (10). */
-constexpr int kPoseScratch = 34;
+/* Scratch floats per pose pair (TPP > 1): rigid m/t of both poses (24), the current
+ * torsion's axis k of both poses (6, padded to 8), then cos/sin of every torsion of both
+ * poses (4 per torsion). */
+constexpr int kPoseScratch = 32;
+__host__ __device__ inline int pose_scratch_floats(int n_tors) { return kPoseScratch + 4 * n_tors; }
 
 /* Build poses g0 -> .x and g1 -> .y of the tile column S (S already offset by pp).
- * TPP > 1: the per-pose fp64 scalars (matrix, torsion axes, sincos) are computed
- * once -- sub 0 for pose 0, sub 1 for pose 1 -- and shared through the scratch
- * column X instead of being replicated by every sub. */
+ * TPP > 1: the per-pose fp64 scalars are computed once and shared through the
+ * scratch column X: sub 0/1 build pose 0/1's matrix and torsion axes (the chain), and
+ * the cos/sin of every torsion angle -- which do not depend on the chain -- are spread
+ * over all subs up front.  CTA barriers order the chain (keeping the TPP subs of a pose
+ * pair in one warp with __syncwarp measured slower: the axis work then runs on half-empty
+ * warps, and the bank-conflict padding it needs cost the GA an occupancy step).  The
+ * caller syncs after the call (TPP > 1); the tile must be free when it is called. */
 template <int NPP, int TPP>
 __device__ __forceinline__ void build_pose2(const LigView &L, const double *__restrict__ g0,
                                             const double *__restrict__ g1, float2 *S, int sub,
@@ -201,7 +207,6 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
 {
 #define VD_X(k) X[(k) * NPP]
     float2 M00, M01, M02, M10, M11, M12, M20, M21, M22, TX, TY, TZ;
-    if (TPP > 1) __syncthreads();  /* S and the scratch may still be read for the previous poses */
     if (TPP == 1) {
         float m0[9], t0[3], m1[9], t1[3];
         rigid_of(g0, m0, t0);
@@ -219,6 +224,14 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
 #pragma unroll
             for (int k = 0; k < 3; ++k) VD_X(12 * sub + 9 + k) = t[k];
         }
+        /* cos/sin of every torsion angle, spread over all subs (they do not depend on
+           the chain): task k = (torsion k >> 1, pose k & 1) */
+        for (int k = sub; k < 2 * L.n_torsions; k += TPP) {
+            double sd, cd;
+            sincos(((k & 1) ? g1 : g0)[7 + (k >> 1)], &sd, &cd);
+            VD_X(kPoseScratch + 4 * (k >> 1) + (k & 1)) = __double2float_rn(cd);
+            VD_X(kPoseScratch + 4 * (k >> 1) + 2 + (k & 1)) = __double2float_rn(sd);
+        }
         __syncthreads();
         M00 = f2(VD_X(0), VD_X(12)); M01 = f2(VD_X(1), VD_X(13)); M02 = f2(VD_X(2), VD_X(14));
         M10 = f2(VD_X(3), VD_X(15)); M11 = f2(VD_X(4), VD_X(16)); M12 = f2(VD_X(5), VD_X(17));
@@ -235,9 +248,9 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
     if (TPP > 1) __syncthreads();
     for (int t = 0; t < L.n_torsions; ++t) {
         const int4 tr = L.tors[t];
-        const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
         float2 KX, KY, KZ, C, SN;
         if (TPP == 1) {
+            const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
             torsion_axis(sub2(VD_S2(tr.y, 0), ox), sub2(VD_S2(tr.y, 1), oy),
                          sub2(VD_S2(tr.y, 2), oz), KX, KY, KZ);
             double s0, c0, s1, c1;
@@ -247,26 +260,23 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
             SN = f2(__double2float_rn(s0), __double2float_rn(s1));
         } else {
             if (sub < 2) {
-                const float ax = __fsub_rn(sub ? VD_S2(tr.y, 0).y : VD_S2(tr.y, 0).x, sub ? ox.y : ox.x);
-                const float ay = __fsub_rn(sub ? VD_S2(tr.y, 1).y : VD_S2(tr.y, 1).x, sub ? oy.y : oy.x);
-                const float az = __fsub_rn(sub ? VD_S2(tr.y, 2).y : VD_S2(tr.y, 2).x, sub ? oz.y : oz.x);
+                const float ax = __fsub_rn(sub ? VD_S2(tr.y, 0).y : VD_S2(tr.y, 0).x, sub ? VD_S2(tr.x, 0).y : VD_S2(tr.x, 0).x);
+                const float ay = __fsub_rn(sub ? VD_S2(tr.y, 1).y : VD_S2(tr.y, 1).x, sub ? VD_S2(tr.x, 1).y : VD_S2(tr.x, 1).x);
+                const float az = __fsub_rn(sub ? VD_S2(tr.y, 2).y : VD_S2(tr.y, 2).x, sub ? VD_S2(tr.x, 2).y : VD_S2(tr.x, 2).x);
                 const double x = (double)ax, y = (double)ay, z = (double)az;
                 const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
-                double sd, cd;
-                sincos((sub ? g1 : g0)[7 + t], &sd, &cd);
-                VD_X(24 + 5 * sub + 0) = __double2float_rn(__ddiv_rn(x, n));
-                VD_X(24 + 5 * sub + 1) = __double2float_rn(__ddiv_rn(y, n));
-                VD_X(24 + 5 * sub + 2) = __double2float_rn(__ddiv_rn(z, n));
-                VD_X(24 + 5 * sub + 3) = __double2float_rn(cd);
-                VD_X(24 + 5 * sub + 4) = __double2float_rn(sd);
+                VD_X(24 + 3 * sub + 0) = __double2float_rn(__ddiv_rn(x, n));
+                VD_X(24 + 3 * sub + 1) = __double2float_rn(__ddiv_rn(y, n));
+                VD_X(24 + 3 * sub + 2) = __double2float_rn(__ddiv_rn(z, n));
             }
             __syncthreads();
-            KX = f2(VD_X(24), VD_X(29));
-            KY = f2(VD_X(25), VD_X(30));
-            KZ = f2(VD_X(26), VD_X(31));
-            C = f2(VD_X(27), VD_X(32));
-            SN = f2(VD_X(28), VD_X(33));
+            KX = f2(VD_X(24), VD_X(27));
+            KY = f2(VD_X(25), VD_X(28));
+            KZ = f2(VD_X(26), VD_X(29));
+            C = f2(VD_X(kPoseScratch + 4 * t + 0), VD_X(kPoseScratch + 4 * t + 1));
+            SN = f2(VD_X(kPoseScratch + 4 * t + 2), VD_X(kPoseScratch + 4 * t + 3));
         }
+        const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
         const float2 OMC = sub2(f2(1.0f), C);
 #pragma unroll 4
         for (int f = tr.z + sub; f < tr.w; f += TPP) {
@@ -722,65 +732,12 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
     }
 }
 
-/* FAST inter + intra interleaved (packed maps, resident pair list): the grid gathers of
- * one atom are issued, then a slice of the pair stream runs while they are in flight, then
- * the atom is interpolated.  The slices are CTA-uniform ranges of the flat pair stream
- * (each split at the 12-6 | 12-10 boundary), so every pair is still visited by exactly
- * one sub of the pose pair with broadcast parameter loads, and no barrier is needed. */
-#ifndef VD_FUSED
-#define VD_FUSED 0
-#endif
-template <int NPP, int TPP>
-__device__ __forceinline__ void fused_fast(const LigView &L, const GridView &G, const float2 *S,
-                                           const PairTile &T, int sub, double &e0, double &e1,
-                                           double &a0, double &a1)
-{
-    const int n = L.n_atoms, np = L.n_pairs, kh = L.n_nohb;
-    const bool cut = L.cut2 < INFINITY;
-    const int nit = (n + TPP - 1) / TPP;  /* CTA-uniform atom iterations */
-    Gather c0, c1;
-    auto issue = [&](int i) {
-        const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
-        const float4 *tz = type_map(G, __float_as_int(L.atom2[i].y));
-        int idx0, idx1;
-        cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0);
-        cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1);
-        issue_packed(G, tz, idx0, c0);
-        issue_packed(G, tz, idx1, c1);
-    };
-    if (sub < n) issue(sub);
-    double s0 = 0.0, s1 = 0.0;
-    for (int it = 0; it < nit; ++it) {
-        const int kb = (int)((int64_t)np * it / nit), ke = (int)((int64_t)np * (it + 1) / nit);
-        const int km = min(ke, max(kb, kh));
-        float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, km, T.coef, T.off, sub, L.cut2)
-                          : flat_fast<NPP, TPP, false, false>(S, kb, km, T.coef, T.off, sub, L.cut2);
-        part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, km, ke, T.coef, T.off, sub, L.cut2)
-                               : flat_fast<NPP, TPP, true, false>(S, km, ke, T.coef, T.off, sub, L.cut2));
-        s0 += (double)part.x;
-        s1 += (double)part.y;
-        const int i = sub + it * TPP;
-        if (i < n) {
-            const float q = L.atom[i].w, dsf = L.atom2[i].x;
-            e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
-            e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
-            if (i + TPP < n) issue(i + TPP);
-        }
-    }
-    a0 = s0;
-    a1 = s1;
-}
-
 /* inter + intra of both poses (all CTA threads must call) */
 template <bool EXACT, int NPP, int TPP>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
                                         double &a0, double &a1)
 {
-    if (VD_FUSED && !EXACT && G.yz != nullptr && T.resident) {
-        fused_fast<NPP, TPP>(L, G, S, T, sub, e0, e1, a0, a1);
-        return;
-    }
     inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
     intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }
@@ -837,7 +794,7 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     off = align16(off + 16u * (unsigned)n_tors);
     s.topo_frag = off;
     off = align16(off + 4u * (unsigned)n_frag);
-    const unsigned scratch_bytes = (tpp > 1) ? 4u * kPoseScratch * (unsigned)npp : 0u;
+    const unsigned scratch_bytes = (tpp > 1) ? 4u * (unsigned)pose_scratch_floats(n_tors) * (unsigned)npp : 0u;
     s.scratch = off;
     off = align16(off + scratch_bytes);
     s.resident = n_pairs <= kResidentPairs;

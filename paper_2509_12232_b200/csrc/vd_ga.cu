@@ -200,10 +200,13 @@ __global__ void __launch_bounds__(NPP *TPP, VD_GA_MINB) ga_kernel(GridView Gv, c
         __syncthreads();
         for (int gen = 0; gen <= P.generations; ++gen) {
             for (int b0 = 0; b0 < pop; b0 += 2 * NPP) {
+                /* the tile is free: the previous energy stage's reads ended at
+                   reduce_subs' first barrier */
                 const int i0 = b0 + 2 * pp, i1 = i0 + 1;
-                const int q0 = min(i0, pop - 1), q1 = min(i1, pop - 1);
-                build_pose2<NPP, TPP>(L, cur + (size_t)q0 * G, cur + (size_t)q1 * G, S, sub,
+                build_pose2<NPP, TPP>(L, cur + (size_t)min(i0, pop - 1) * G,
+                                      cur + (size_t)min(i1, pop - 1) * G, S, sub,
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
+                if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 energy2<EXACT, NPP, TPP>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
@@ -385,7 +388,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         }
         Launch L;
         int npp0;
-        if (vd::pick_shape(nmax, pmax, exact, &npp0, &L.tpp)) return -1;
+        if (vd::pick_shape(nmax, pmax, tb, exact, &npp0, &L.tpp)) return -1;
         /* pose-pairs per CTA: the candidate with most resident warps per SM
            (VD_GA_NPP forces one, for tuning) */
         int best_warps = -1;

@@ -53,7 +53,7 @@ bool make_packed(vd_grid *g);
 }  // namespace vdi
 
 namespace vd {
-int pick_shape(int n_atoms, int n_pairs, bool exact, int *npp, int *tpp);
+int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp);
 }
 
 #define VD_CK(call)                                        \

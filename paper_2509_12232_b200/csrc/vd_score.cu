@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     if (genes) {
         build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
                               reinterpret_cast<float *>(smem + lay.scratch) + pp);
+        if (TPP > 1) __syncthreads();
     } else {
         const int n = L.n_atoms;
         const float *s0 = poses + q0 * 3 * n, *s1 = poses + q1 * 3 * n;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
 }
 
 /* Launch shape for a ligand: pose pairs per CTA (NPP) and threads per pair (TPP). */
-int pick_shape(int n_atoms, int n_pairs, bool exact, int *npp, int *tpp)
+int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp)
 {
     const unsigned limit = 200 * 1024;
     /* threads per pose pair: more subs for larger ligands, where 12*N bytes of
@@ -105,7 +106,7 @@ int pick_shape(int n_atoms, int n_pairs, bool exact, int *npp, int *tpp)
     const int pref_fast[3] = {32, 16, 64}, pref_exact[3] = {64, 32, 16};
     for (int n : (exact ? pref_exact : pref_fast)) {
         if (force_npp && n != force_npp) continue;
-        if (smem_layout(n_atoms, 64, 4 * n_atoms, n, t, 0, n_pairs).bytes <= limit) {
+        if (smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes <= limit) {
             *npp = n;
             *tpp = t;
             return 0;
@@ -139,7 +140,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
 {
     const bool exact = mode == VD_MODE_EXACT;
     int npp, tpp;
-    if (pick_shape(L.n_atoms, L.n_pairs, exact, &npp, &tpp)) return cudaErrorInvalidValue;
+    if (pick_shape(L.n_atoms, L.n_pairs, L.n_torsions, exact, &npp, &tpp)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
     const double *g = src == 0 ? genes : nullptr;
     const float *p = src == 0 ? nullptr : poses;
@@ -158,7 +159,7 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
                         cudaStream_t st)
 {
     int npp, tpp;
-    if (pick_shape(L.n_atoms, 0, true, &npp, &tpp)) return cudaErrorInvalidValue;
+    if (pick_shape(L.n_atoms, 0, L.n_torsions, true, &npp, &tpp)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
     const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, 1, 0, 0);
     const size_t smem = lay.bytes;
