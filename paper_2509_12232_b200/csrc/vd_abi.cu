@@ -69,12 +69,18 @@ __global__ void pack_yz(const float *__restrict__ maps, int64_t n, int ny, int n
     }
 }
 
-__global__ void pack_z(const float *__restrict__ maps, int64_t n, int nz, float2 *zp)
+/* zy layout: z-pair (v[z], v[z+1]) of node (x, y, z) at ((x*nyp + y/2)*nz + z)*2 + (y&1) */
+__global__ void pack_zy(const float *__restrict__ maps, int64_t n, int ny, int nz, float2 *zp)
 {
+    const int nyp = (ny + 1) / 2;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
-        const bool zl = (k % nz) == nz - 1;
-        zp[k] = make_float2(maps[k], zl ? 0.f : maps[k + 1]);
+        const int z = (int)(k % nz);
+        const int64_t xy = k / nz;
+        const int y = (int)(xy % ny);
+        const int64_t x = xy / ny;
+        zp[((x * nyp + (y >> 1)) * nz + z) * 2 + (y & 1)] =
+            make_float2(maps[k], z == nz - 1 ? 0.f : maps[k + 1]);
     }
 }
 
@@ -99,14 +105,20 @@ bool make_packed(vd_grid *g)
 {
     const int64_t nodes = (int64_t)g->nx * g->ny * g->nz;
     const int64_t n_type = g->n_maps > 2 ? g->n_maps - 2 : 1;
-    const int64_t brick = nodes * (16 * n_type + 32), zpair = nodes * (8 * n_type + 32);
+    const int64_t zy_nodes = (int64_t)g->nx * (2 * ((g->ny + 1) / 2)) * g->nz;
+    const int64_t brick = nodes * (16 * n_type + 32), zpair = zy_nodes * 8 * n_type + nodes * 32;
     if (getenv("VD_NO_PACK") || zpair > (int64_t)96 << 20) return true;
     const char *ov = getenv("VD_BRICK_BUDGET_MB");  /* tests force either layout */
     g->zpair = brick > ((ov ? atoll(ov) : (int64_t)VD_BRICK_BUDGET_MB) << 20);
     /* type maps are packed lazily in ed_for(): only the maps a ligand set can
        reference (every map except its elec/desolv pair) */
     g->yz_packed.assign(g->n_maps, 0);
-    return check(cudaMalloc(&g->d_yz, (g->zpair ? sizeof(float2) : sizeof(float4)) * nodes * g->n_maps), "alloc yz");
+    g->tstride = g->zpair ? zy_nodes : nodes;
+    if (!check(cudaMalloc(&g->d_yz, (g->zpair ? sizeof(float2) : sizeof(float4)) * g->tstride * g->n_maps), "alloc yz"))
+        return false;
+    /* zy rows past ny (odd ny) are never read as corners but are gathered as the 2nd
+       half of a 16-B group: keep them defined */
+    return check(cudaMemset(g->d_yz, 0, (g->zpair ? sizeof(float2) : sizeof(float4)) * g->tstride * g->n_maps), "zero yz");
 }
 
 static const float4 *ed_for(const vd_grid *gc, int e, int d)
@@ -126,10 +138,10 @@ static const float4 *ed_for(const vd_grid *gc, int e, int d)
     for (int m = 0; m < g->n_maps; ++m)
         if (m != e && m != d && !g->yz_packed[m]) {
             if (g->zpair)
-                pack_z<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->nz,
-                                      reinterpret_cast<float2 *>(g->d_yz) + nodes * m);
+                pack_zy<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->ny, g->nz,
+                                       reinterpret_cast<float2 *>(g->d_yz) + g->tstride * m);
             else
-                pack_yz<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->ny, g->nz, g->d_yz + nodes * m);
+                pack_yz<<<1184, 256>>>(g->d_maps + nodes * m, nodes, g->ny, g->nz, g->d_yz + g->tstride * m);
             g->yz_packed[m] = 1;
         }
     if (cudaDeviceSynchronize() != cudaSuccess) {
@@ -156,6 +168,8 @@ vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)
     v.spacing = g->spacing;
     v.one = 1.0f;
     v.zpair = g->zpair ? 1 : 0;
+    v.nyp = (g->ny + 1) / 2;
+    v.tstride = g->tstride;
     return v;
 }
 

@@ -17,7 +17,8 @@ struct vd_grid {
     float lo[3], hi[3], spacing;
     float *d_maps;           /* (n_maps, nx, ny, nz) */
     float4 *d_yz;            /* packed type maps (yz-bricks or z-pairs), or null (see GridView) */
-    bool zpair;              /* d_yz holds z-pairs (8 B/node) instead of yz-bricks (16 B/node) */
+    bool zpair;              /* d_yz holds zy z-pairs (8 B/node) instead of yz-bricks (16 B/node) */
+    int64_t tstride;         /* elements per packed type map */
     std::vector<char> yz_packed;
     std::mutex ed_lock;
     std::map<std::pair<int, int>, float4 *> d_ed;  /* packed (elec, desolv) per map pair */
