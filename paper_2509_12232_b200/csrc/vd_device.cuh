@@ -486,9 +486,11 @@ __device__ __forceinline__ float atom_term(const GridView &G, const float *__res
 }
 
 /* inter of both poses over this sub's atoms; EXACT requires TPP == 1 (atom order).
- * Packed layout: software-pipelined, the gathers of atom i+TPP are in flight
- * while atom i is interpolated. */
-template <bool EXACT, int NPP, int TPP>
+ * PIPE (packed layout): software-pipelined, the gathers of atom i+TPP are in flight while
+ * atom i is interpolated.  That doubles the live gather state (152 vs 94 registers in
+ * score_kernel); the score kernel runs unpipelined and covers the latency with its 12
+ * resident warps, the GA kernel (register-bound by its other stages anyway) pipelines. */
+template <bool EXACT, int NPP, int TPP, bool PIPE>
 __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, const float2 *S,
                                        int sub, double &e0, double &e1)
 {
@@ -509,6 +511,11 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
         for (; i < n; i += TPP) {
             const int in = i + TPP;
             Gather n0, n1;
+            if (!PIPE) {
+                const float q = L.atom[i].w, dsf = L.atom2[i].x;
+                e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
+                e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
+            }
             if (in < n) {
                 const float2 x = VD_S2(in, 0), y = VD_S2(in, 1), z = VD_S2(in, 2);
                 const float4 *tz = type_map(G, __float_as_int(L.atom2[in].y));
@@ -518,9 +525,11 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
                 issue_packed(G, tz, idx0, zy0, n0);
                 issue_packed(G, tz, idx1, zy1, n1);
             }
-            const float q = L.atom[i].w, dsf = L.atom2[i].x;
-            e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
-            e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
+            if (PIPE) {
+                const float q = L.atom[i].w, dsf = L.atom2[i].x;
+                e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
+                e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
+            }
             c0 = n0;
             c1 = n1;
         }
@@ -639,6 +648,40 @@ __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, con
     return acc;
 }
 
+/* The same sum with i-reuse: each sub walks one contiguous quarter of [kb, ke) (the fast
+ * order is row-major inside each hb group, so i stays constant over runs of ~N/2 pairs)
+ * and reloads atom i's coordinates only when i changes -- a warp-uniform test, since all
+ * lanes of a warp process the same pair.  Per pair that is 3 LDS.64 of the j atom instead
+ * of 6: the shared-memory wavefronts of this loop were the largest user of the L1 data
+ * pipe the grid gathers also need. */
+#ifndef VD_INTRA_ROWS
+#define VD_INTRA_ROWS 1
+#endif
+template <int NPP, int TPP, bool HB, bool CUT>
+__device__ __forceinline__ float2 rows_fast(const float2 *S, int kb, int ke, const float4 *tc,
+                                            const int2 *toff, int sub, float cut2)
+{
+    const int n = ke - kb;
+    const int k0 = kb + (n * sub) / TPP, k1 = kb + (n * (sub + 1)) / TPP;
+    float2 acc = f2(0.0f), xi = f2(0.0f), yi = f2(0.0f), zi = f2(0.0f);
+    int ci = -1;
+#pragma unroll kFlatUnroll
+    for (int k = k0; k < k1; ++k) {
+        const float4 c = tc[k];
+        const int2 o = toff[k];
+        if (o.x != ci) {
+            ci = o.x;
+            xi = S[o.x];
+            yi = S[o.x + NPP];
+            zi = S[o.x + 2 * NPP];
+        }
+        const float2 *Sj = S + o.y;
+        acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(xi, Sj[0]), fsub2(yi, Sj[NPP]),
+                                             fsub2(zi, Sj[2 * NPP]), c, cut2));
+    }
+    return acc;
+}
+
 /* Shared-memory pair area (per CTA): the whole list (resident) or one tile. */
 struct PairTile {
     float4 *coef;   /* [cap] weight-folded a, b, qq, dsl */
@@ -739,10 +782,17 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
             for (int c0 = 0; c0 < tcnt; c0 += kTile) {
                 const int kb = c0, ke = min(tcnt, c0 + kTile);
                 const int kh = min(ke, max(kb, L.n_nohb - t0));  /* 12-6 | 12-10 boundary */
+#if VD_INTRA_ROWS
+                float2 part = cut ? rows_fast<NPP, TPP, false, true>(S, kb, kh, T.coef, T.off, sub, L.cut2)
+                                  : rows_fast<NPP, TPP, false, false>(S, kb, kh, T.coef, T.off, sub, L.cut2);
+                part = fadd2(part, cut ? rows_fast<NPP, TPP, true, true>(S, kh, ke, T.coef, T.off, sub, L.cut2)
+                                       : rows_fast<NPP, TPP, true, false>(S, kh, ke, T.coef, T.off, sub, L.cut2));
+#else
                 float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, kh, T.coef, T.off, sub, L.cut2)
                                   : flat_fast<NPP, TPP, false, false>(S, kb, kh, T.coef, T.off, sub, L.cut2);
                 part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, ke, T.coef, T.off, sub, L.cut2)
                                        : flat_fast<NPP, TPP, true, false>(S, kh, ke, T.coef, T.off, sub, L.cut2));
+#endif
                 s0 += (double)part.x;
                 s1 += (double)part.y;
             }
@@ -753,12 +803,12 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
 }
 
 /* inter + intra of both poses (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP>
+template <bool EXACT, int NPP, int TPP, bool PIPE>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
                                         double &a0, double &a1)
 {
-    inter2<EXACT, NPP, TPP>(L, G, S, sub, e0, e1);
+    inter2<EXACT, NPP, TPP, PIPE>(L, G, S, sub, e0, e1);
     intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }
 
@@ -823,9 +873,12 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     off += 16u * (unsigned)s.cap;
     s.tile_idx = off;
     off = align16(off + 8u * (unsigned)s.cap);
-    /* the sub reduction reuses a streamed tile (intra is finished when it runs) */
+    /* the sub reduction reuses the pose scratch (the pose stage is over when it runs;
+       the GA syncs before the next tile's pose stage) or a streamed pair tile */
     const unsigned red_bytes = (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
-    if (!s.resident && red_bytes <= 24u * (unsigned)s.cap) {
+    if (red_bytes <= scratch_bytes) {
+        s.red = s.scratch;
+    } else if (!s.resident && red_bytes <= 24u * (unsigned)s.cap) {
         s.red = s.tile_coef;
     } else {
         s.red = off;

@@ -200,15 +200,17 @@ __global__ void __launch_bounds__(NPP *TPP, VD_GA_MINB) ga_kernel(GridView Gv, c
         __syncthreads();
         for (int gen = 0; gen <= P.generations; ++gen) {
             for (int b0 = 0; b0 < pop; b0 += 2 * NPP) {
-                /* the tile is free: the previous energy stage's reads ended at
-                   reduce_subs' first barrier */
+                /* the tile is free (the previous energy stage's reads ended at
+                   reduce_subs' first barrier), the scratch once sub 0 has read the
+                   reduction it holds */
+                if (TPP > 1 && b0 > 0) __syncthreads();
                 const int i0 = b0 + 2 * pp, i1 = i0 + 1;
                 build_pose2<NPP, TPP>(L, cur + (size_t)min(i0, pop - 1) * G,
                                       cur + (size_t)min(i1, pop - 1) * G, S, sub,
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, true>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }

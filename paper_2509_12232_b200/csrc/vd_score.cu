@@ -7,6 +7,7 @@
  * vd/scoring/__init__.py:345.  A CTA owns 2*NPP poses (NPP pose pairs, TPP
  * threads per pair); see vd_device.cuh for the stage contracts.
  */
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
         if (TPP > 1) __syncthreads();
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-    energy2<EXACT, NPP, TPP>(L, G, S, T, sub, e0, e1, a0, a1);
+    energy2<EXACT, NPP, TPP, false>(L, G, S, T, sub, e0, e1, a0, a1);
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
@@ -125,6 +126,21 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0, L.n_pairs);
     auto k = score_kernel<EXACT, NPP, TPP>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+    if (e != cudaSuccess) return e;
+    /* Shared-memory carveout: just enough for min(occupancy, 12 warps) CTAs per SM, the
+       rest stays L1 for the grid gathers (an atom's corners share lines with its bonded
+       neighbours').  cfg1 A/B: 1.77 ms at 3 CTAs + max L1 vs 2.00 ms at 4 CTAs (the
+       driver's occupancy-maximising default) and 2.20 ms at 2 CTAs. */
+    int occ = 0, dev = 0, smem_sm = 0, resv = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NPP * TPP, lay.bytes);
+    if (e != cudaSuccess) return e;
+    const int want = std::max(1, std::min(occ, 384 / (NPP * TPP)));
+    int pct = (int)((100LL * want * (lay.bytes + resv) + smem_sm - 1) / smem_sm);
+    if (const char *cv = getenv("VD_CARVEOUT")) pct = atoi(cv);  /* tuning override */
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(100, pct));
     if (e != cudaSuccess) return e;
     const int64_t per_cta = 2 * NPP;
     const int64_t blocks = (P + per_cta - 1) / per_cta;
