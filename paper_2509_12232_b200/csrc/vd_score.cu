@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
         }
 }
 
+constexpr unsigned kL1ReserveKB = 32;  /* of the 256 KB L1/shared array, kept as L1 */
+
 /* Launch shape for a ligand: pose pairs per CTA (NPP) and threads per pair (TPP). */
 int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp)
 {
@@ -102,17 +104,23 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
     int force_npp = 0;
     if (!exact)
         if (const char *ov = getenv("VD_NPP")) force_npp = atoi(ov);  /* tuning override */
-    /* fast mode prefers 32 pose pairs x 4 threads (cfg1 A/B on B200: 2.16 ms vs
-       2.44 ms for NPP=64 even though NPP=64 keeps 16 vs 12 warps resident) */
-    const int pref_fast[3] = {32, 16, 64}, pref_exact[3] = {64, 32, 16};
-    for (int n : (exact ? pref_exact : pref_fast)) {
-        if (force_npp && n != force_npp) continue;
-        if (smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes <= limit) {
-            *npp = n;
-            *tpp = t;
-            return 0;
+    /* pose pairs per CTA: the largest tile of which 2 CTAs fit beside the L1 share kept
+       for the gathers (see launch_t), else the first that fits at all.  cfg1 sweep
+       (TPP x NPP, CTAs/SM): 4 x 64 (2) 1.67 ms; 4 x 32 (3) 1.77; 8 x 16 (6) 1.85;
+       4 x 128 (1) 1.92; 2 x 64 (2) 1.99.  A bigger tile amortises the shared pair list
+       over more poses, so more poses are resident per SM at the same L1 share. */
+    const unsigned two_ctas = (228u - kL1ReserveKB) * 1024u / 2u - 1024u;
+    for (int pass = 0; pass < 2; ++pass)
+        for (int n : {64, 32, 16}) {
+            if (force_npp && n != force_npp) continue;
+            if (!exact && pass == 0 && n == 16) continue;
+            const unsigned b = smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes;
+            if (b <= (pass == 0 && !exact ? two_ctas : limit)) {
+                *npp = n;
+                *tpp = t;
+                return 0;
+            }
         }
-    }
     vdi::set_error("ligand too large for the shared-memory pose tile (n_atoms = " +
                    std::to_string(n_atoms) + ")");
     return -1;
@@ -127,17 +135,20 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     auto k = score_kernel<EXACT, NPP, TPP>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
     if (e != cudaSuccess) return e;
-    /* Shared-memory carveout: just enough for min(occupancy, 12 warps) CTAs per SM, the
-       rest stays L1 for the grid gathers (an atom's corners share lines with its bonded
-       neighbours').  cfg1 A/B: 1.77 ms at 3 CTAs + max L1 vs 2.00 ms at 4 CTAs (the
-       driver's occupancy-maximising default) and 2.20 ms at 2 CTAs. */
+    /* Shared-memory carveout: as many CTAs per SM as fit while >= 32 KB of the 256 KB
+       L1/shared array stays L1 for the grid gathers (an atom's corners share lines with
+       its bonded neighbours').  cfg1 A/B, NPP 32: 1.77 ms at 3 CTAs (63 KB L1) vs 2.00 ms
+       at 4 (8 KB L1, the driver's occupancy-maximising default); NPP 64: 1.67 ms at 2. */
     int occ = 0, dev = 0, smem_sm = 0, resv = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NPP * TPP, lay.bytes);
     if (e != cudaSuccess) return e;
-    const int want = std::max(1, std::min(occ, 384 / (NPP * TPP)));
+    int l1_kb = kL1ReserveKB;
+    if (const char *w = getenv("VD_L1_KB")) l1_kb = atoi(w);  /* tuning override */
+    const int fit = (smem_sm - l1_kb * 1024) / (int)(lay.bytes + resv);
+    const int want = std::max(1, std::min(occ, fit));
     int pct = (int)((100LL * want * (lay.bytes + resv) + smem_sm - 1) / smem_sm);
     if (const char *cv = getenv("VD_CARVEOUT")) pct = atoi(cv);  /* tuning override */
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(100, pct));
@@ -167,6 +178,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
     VD_L(false, 64, 2); VD_L(false, 32, 2); VD_L(false, 16, 2);
     VD_L(false, 64, 4); VD_L(false, 32, 4); VD_L(false, 16, 4);
     VD_L(false, 32, 8); VD_L(false, 16, 8);
+    VD_L(false, 64, 8);
 #undef VD_L
     return cudaErrorInvalidConfiguration;
 }
