@@ -42,8 +42,8 @@ WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
 # dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
 # committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
-TRAFFIC_BYTES = 165.56e6 + 21.00e6
-TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,32,4,1>)"
+TRAFFIC_BYTES = 165.87e6 + 20.92e6
+TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,64,4>)"
 
 
 def env_int(k, d):
@@ -115,7 +115,7 @@ def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx
             "ceiling_poses_per_s": fp32_peak * 1e12 / fpp}
     out = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
            "frac": achieved_tf / fp32_peak, "traffic": TRAFFIC_BYTES,
-           "traffic_source": TRAFFIC_SRC, "kernel": "vd::score_kernel<false,32,4>",
+           "traffic_source": TRAFFIC_SRC, "kernel": "vd::score_kernel<false,64,4>",
            "fp32": fp32, "arithmetic_intensity_flop_per_byte": fpp / bpp}
     if peaks:
         l2 = peaks["l2_gather_gbs"]
@@ -392,6 +392,9 @@ def screening_leg(args, rank, world, dist, dev):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     evals = n * ga.population_size * (ga.generations + 1)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        cpu = cpu_screen_baseline(gset, batch, ga, lo, args.cpu_seconds)
     from paper_2509_12232_b200 import benchrecords as br
 
     npairs = float(arrays["pair_start"][-1]) / max(1, count)
@@ -403,8 +406,49 @@ def screening_leg(args, rank, world, dist, dev):
             "workload": "cfg2-screen-10k" if n == 10000 else f"cfg2-distribution x{n}",
             "gathered_records": int(rec.shape[0]), "gather_ms": round(1e3 * t_gather, 3),
             "host_prep_s_per_rank": round(prep_s, 3),
-            "timing": "CUDA events around the one persistent GA launch, max over ranks",
+            "timing": "CUDA events around vd_dock_batch (one persistent GA launch per atom-count bucket, buckets concurrent), max over ranks",
+            **({"cpu_baseline": cpu} if cpu else {}),
             "_modeled": modeled}
+
+
+def cpu_screen_baseline(gset, batch, ga, index_base, seconds=10.0):
+    """The reference GA + scoring on the host (oracle/vd_ga_oracle.c: the restated GA, the
+    same per-ligand keys as the device, OpenMP over ligands) on the first ligands of the
+    screening batch, bounded to ~`seconds`: ligands docked/s on all host threads."""
+    from oracle import oracle
+    from paper_2509_12232_b200 import chem
+    from paper_2509_12232_b200.context import prepare_context
+
+    labels = list(gset.maps)
+    gidx = {l: k for k, l in enumerate(labels)}
+    stack = np.stack([gset.maps[l] for l in labels]).astype(np.float32)
+    cores = oracle.cores()
+    params = oracle.ga_params(ga, gset.spec.origin, gset.spec.upper)
+
+    def ligs(a, b):
+        out = []
+        for l in range(a, b):
+            ctx = prepare_context(batch.topology(l), gset)
+            amap = np.array([gidx[ctx.map_labels[k]] for k in ctx.atom_slot], np.int32)
+            out.append(oracle.Ligand(ctx, stack, amap, gidx[chem.ELEC_LABEL],
+                                     gidx[chem.DESOLV_LABEL]))
+        return out
+
+    k = min(len(batch), cores)  # probe: one ligand per thread
+    t0 = time.perf_counter()
+    oracle.dock_many(ligs(0, k), params, 0, index_base, n_threads=cores)
+    rate = k / max(time.perf_counter() - t0, 1e-9)
+    m = int(min(len(batch) - k, max(cores, rate * seconds)))
+    if m <= 0:
+        m, k = k, 0
+    sample = ligs(k, k + m)
+    t0 = time.perf_counter()
+    oracle.dock_many(sample, params, 0, index_base + k, n_threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": m / dt, "unit": "ligands/s", "cores": cores, "kind": "port",
+            "sample": f"ligands {k}..{k + m - 1} of the cfg2 batch, pop {ga.population_size} x "
+                      f"{ga.generations} generations, {dt:.1f} s on {cores} threads "
+                      "(oracle/vd_ga_oracle.c restated GA + oracle/vd_oracle.c scoring)"}
 
 
 def cpu_baseline(ctx, genes, seconds=10.0):

@@ -158,8 +158,19 @@ struct GaLayout {
 #ifndef VD_GA_MINB
 #define VD_GA_MINB 1
 #endif
+#ifndef VD_GA_PIPE
+#define VD_GA_PIPE 1   /* software-pipelined grid gathers (see inter2) */
+#endif
+#ifndef VD_GA_REGS
+#define VD_GA_REGS 0   /* >0: register cap per thread (min resident CTAs derived from it) */
+#endif
+constexpr int ga_minb(int threads)
+{
+    return VD_GA_REGS > 0 ? (65536 / (threads * VD_GA_REGS) > 0 ? 65536 / (threads * VD_GA_REGS) : 1)
+                          : VD_GA_MINB;
+}
 template <bool EXACT, int NPP, int TPP>
-__global__ void __launch_bounds__(NPP *TPP, VD_GA_MINB) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+__global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, int count,
                                                       GaDev P, uint64_t seed, int64_t base,
                                                       int *work, double *gene_buf, int gmax,
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(NPP *TPP, VD_GA_MINB) ga_kernel(GridView Gv, c
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, true>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
@@ -391,6 +402,11 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         Launch L;
         int npp0;
         if (vd::pick_shape(nmax, pmax, tb, exact, &npp0, &L.tpp)) return -1;
+        if (!exact)
+            if (const char *ov = getenv("VD_GA_TPP")) {  /* tuning override */
+                const int v = atoi(ov);
+                if (v == 1 || v == 2 || v == 4 || v == 8) L.tpp = v;
+            }
         /* pose-pairs per CTA: the candidate with most resident warps per SM
            (VD_GA_NPP forces one, for tuning) */
         int best_warps = -1;
@@ -459,14 +475,40 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     o.best_total = d_bt; o.best_inter = d_be; o.best_intra = d_ba; o.best_genes = d_bg;
     o.gstride = gstride; o.trace = d_tr; o.n_evals = d_ne;
     const vd::GridView gv = vdi::grid_view(g, s->elec_map, s->desolv_map);
-    for (size_t b = 0; b < launches.size(); ++b) {
+    /* Buckets run concurrently, largest atoms first, each on its own stream forked from st:
+       a persistent launch ends with a tail of SMs whose CTAs found the work counter empty,
+       and the next bucket's CTAs fill them instead of waiting for the whole launch to drain.
+       VD_GA_SERIAL=1 keeps the buckets serial on st (A/B). */
+    const bool serial = getenv("VD_GA_SERIAL") && atoi(getenv("VD_GA_SERIAL")) != 0;
+    std::vector<cudaStream_t> side;
+    cudaEvent_t fork = nullptr;
+    if (!serial && launches.size() > 1) {
+        VD_CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        VD_CK(cudaEventRecord(fork, st));
+    }
+    for (int b = (int)launches.size() - 1; b >= 0; --b) {
         const Launch &L = launches[b];
+        cudaStream_t ls = st;
+        if (fork && b != (int)launches.size() - 1) {
+            VD_CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
+            side.push_back(ls);
+            VD_CK(cudaStreamWaitEvent(ls, fork, 0));
+        }
         int n_ctas = 0;
         gene_buf = nullptr;
         VD_CK(vd::launch_ga(exact, L.npp, L.tpp, gv, d_views, d_order + L.off, L.cnt, P, seed,
-                            lig_index_base, gmax, L.lay, o, st, d_work + b, &gene_buf, &n_ctas));
-        cudaFreeAsync(gene_buf, st);
+                            lig_index_base, gmax, L.lay, o, ls, d_work + b, &gene_buf, &n_ctas));
+        cudaFreeAsync(gene_buf, ls);
     }
+    for (cudaStream_t ls : side) {  /* join: st waits for every side stream */
+        cudaEvent_t done;
+        VD_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        VD_CK(cudaEventRecord(done, ls));
+        VD_CK(cudaStreamWaitEvent(st, done, 0));
+        cudaEventDestroy(done);
+        cudaStreamDestroy(ls);  /* released once its work completes */
+    }
+    if (fork) cudaEventDestroy(fork);
     if (!dev_out) {
         VD_CK(cudaMemcpyAsync(best_total, d_bt, sizeof(float) * count, cudaMemcpyDeviceToHost, st));
         VD_CK(cudaMemcpyAsync(best_inter, d_be, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
