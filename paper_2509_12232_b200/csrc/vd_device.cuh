@@ -771,12 +771,36 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
         const bool cut = L.cut2 < INFINITY;
         double s0 = 0.0, s1 = 0.0;
         const int step = T.resident ? n : T.cap;
+        /* streamed lists: the next tile's coefficients are loaded into registers while the
+           current tile is computed, so the L2 latency of the staging loads stays hidden */
+        constexpr int kPre = (kTile + NPP * TPP - 1) / (NPP * TPP);
+        float4 pc[kPre];
+        int pw[kPre];
+        auto prefetch = [&](int k0) {
+#pragma unroll
+            for (int r = 0; r < kPre; ++r) {
+                const int k = k0 + (int)threadIdx.x + r * NPP * TPP;
+                if ((int)threadIdx.x + r * NPP * TPP < kTile && k < n) {
+                    pc[r] = __ldg(&L.fcoef[k]);
+                    pw[r] = __ldg(&L.fij[k]);
+                }
+            }
+        };
+        if (!T.resident) prefetch(0);
         for (int t0 = 0; t0 < n; t0 += step) {
             const int tcnt = min(step, n - t0);
             if (!T.resident) {
                 __syncthreads();
-                stage_pairs<false, NPP>(L, T, t0, tcnt);
+#pragma unroll
+                for (int r = 0; r < kPre; ++r) {
+                    const int k = (int)threadIdx.x + r * NPP * TPP;
+                    if (k < tcnt) {
+                        T.coef[k] = pc[r];
+                        T.off[k] = make_int2(3 * NPP * (pw[r] & 0xffff), 3 * NPP * (pw[r] >> 16));
+                    }
+                }
                 __syncthreads();
+                if (t0 + step < n) prefetch(t0 + step);
             }
             /* fp32 partials per kTile chunk, flushed to fp64 */
             for (int c0 = 0; c0 < tcnt; c0 += kTile) {

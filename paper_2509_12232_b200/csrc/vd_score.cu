@@ -99,7 +99,7 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
     if (!exact)
         if (const char *ov = getenv("VD_TPP")) {  /* tuning override: 1, 2 or 4 */
             const int v = atoi(ov);
-            if (v == 1 || v == 2 || v == 4 || v == 8) t = v;
+            if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) t = v;
         }
     int force_npp = 0;
     if (!exact)
@@ -179,6 +179,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
     VD_L(false, 64, 4); VD_L(false, 32, 4); VD_L(false, 16, 4);
     VD_L(false, 32, 8); VD_L(false, 16, 8);
     VD_L(false, 64, 8);
+    VD_L(false, 32, 16); VD_L(false, 16, 16);
 #undef VD_L
     return cudaErrorInvalidConfiguration;
 }
