@@ -15,6 +15,7 @@
  * Philox4x64-10 with IEEE-exact transforms, identical to the CPU oracle's.
  */
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -416,8 +417,12 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             vd::GaLayout lay;
             lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra, pmax);
             if (lay.base.bytes > 227u * 1024u) continue;
+            if (npp * L.tpp < 32) continue;  /* block_argmin's shuffles need whole warps */
             int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes) * npp * L.tpp / 32;
             if (npp == 64) warps -= 4;  /* measured: 64 needs clearly more warps to win */
+            /* (unlike the score kernel, the GA prefers one 32 x 8 CTA to two 16 x 8 ones at
+               the same warps for cfg4: 1239 vs 880 ligands/s -- its per-tile barriers and
+               pair-tile streaming are amortised over twice the poses) */
             if (warps > best_warps) {
                 best_warps = warps;
                 L.npp = npp;
@@ -428,6 +433,9 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
             return -1;
         }
+        if (getenv("VD_VERBOSE"))
+            fprintf(stderr, "[vd] ga bucket <=%d atoms: %zu ligands, npp=%d tpp=%d smem=%u warps/sm=%d\n",
+                    kBucketEdge[b], v.size(), L.npp, L.tpp, L.lay.base.bytes, best_warps);
         unsigned off = L.lay.base.extra;
         L.lay.off_e = off;
         off += 8u * p->pop;

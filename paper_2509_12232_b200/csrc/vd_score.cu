@@ -108,12 +108,14 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
        for the gathers (see launch_t), else the first that fits at all.  cfg1 sweep
        (TPP x NPP, CTAs/SM): 4 x 64 (2) 1.67 ms; 4 x 32 (3) 1.77; 8 x 16 (6) 1.85;
        4 x 128 (1) 1.92; 2 x 64 (2) 1.99.  A bigger tile amortises the shared pair list
-       over more poses, so more poses are resident per SM at the same L1 share. */
+       over more poses, so more poses are resident per SM at the same L1 share.  cfg4
+       (128 atoms): 8 x 16 (2 CTAs) 45.5 M poses/s vs 8 x 32 (1 CTA, same warps) 39.9 --
+       a lone CTA idles the SM at every torsion-chain barrier; 8 x 16 with no L1 share
+       (3 CTAs) 28.4: the plain-layout gathers need the L1. */
     const unsigned two_ctas = (228u - kL1ReserveKB) * 1024u / 2u - 1024u;
     for (int pass = 0; pass < 2; ++pass)
         for (int n : {64, 32, 16}) {
             if (force_npp && n != force_npp) continue;
-            if (!exact && pass == 0 && n == 16) continue;
             const unsigned b = smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes;
             if (b <= (pass == 0 && !exact ? two_ctas : limit)) {
                 *npp = n;
@@ -155,6 +157,9 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     if (e != cudaSuccess) return e;
     const int64_t per_cta = 2 * NPP;
     const int64_t blocks = (P + per_cta - 1) / per_cta;
+    if (getenv("VD_VERBOSE"))
+        fprintf(stderr, "[vd] score_kernel<%d,%d,%d> N=%d P=%d smem=%u ctas/sm=%d carveout=%d%%\n",
+                (int)EXACT, NPP, TPP, L.n_atoms, L.n_pairs, lay.bytes, want, pct);
     k<<<(unsigned)blocks, NPP * TPP, lay.bytes, st>>>(G, L, genes, poses, P, ngenes, lay, inter,
                                                         intra, total);
     ++vdi::g_launches;
