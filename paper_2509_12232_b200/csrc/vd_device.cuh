@@ -654,6 +654,9 @@ __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, con
  * lanes of a warp process the same pair.  Per pair that is 3 LDS.64 of the j atom instead
  * of 6: the shared-memory wavefronts of this loop were the largest user of the L1 data
  * pipe the grid gathers also need. */
+#ifndef VD_ROLE_NI8
+#define VD_ROLE_NI8 4   /* gather subs per 8 subs in the role-split energy stage */
+#endif
 #ifndef VD_INTRA_ROWS
 #define VD_INTRA_ROWS 1
 #endif
@@ -827,11 +830,24 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
 }
 
 /* inter + intra of both poses (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP, bool PIPE>
+template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
                                         double &a0, double &a1)
 {
+    /* SPLIT: the first NI = TPP * VD_ROLE_NI8 / 8 subs gather (L1TEX-bound) while the
+       others run the pair sum (MUFU-bound) at the same time, so the two units overlap inside
+       one CTA instead of only across CTAs.  Resident pair lists only (the streamed path has
+       CTA barriers).  cfg1: 1.603 vs 1.683 ms (NI = 2 of 4); NI = 1 or 3 of 4: 2.23 / 1.76 ms.
+       The GA does not split (7,022 vs 8,621 ligands/s): it pipelines its gathers instead. */
+    constexpr int NI = TPP * VD_ROLE_NI8 / 8 > 0 ? TPP * VD_ROLE_NI8 / 8 : 1;
+    if (SPLIT && !EXACT && TPP >= 4 && NI < TPP && T.resident) {
+        if (sub < NI)
+            inter2<EXACT, NPP, NI, PIPE>(L, G, S, sub, e0, e1);
+        else
+            intra2<EXACT, NPP, (TPP - NI > 0 ? TPP - NI : 1)>(L, S, T, sub - NI, a0, a1);
+        return;
+    }
     inter2<EXACT, NPP, TPP, PIPE>(L, G, S, sub, e0, e1);
     intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }

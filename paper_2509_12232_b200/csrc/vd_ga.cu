@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridVie
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, false>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }

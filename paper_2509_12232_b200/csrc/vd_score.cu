@@ -13,6 +13,10 @@
 
 #include "vd_internal.h"
 
+#ifndef VD_SCORE_SPLIT
+#define VD_SCORE_SPLIT 1   /* role-split energy stage (see energy2) */
+#endif
+
 namespace vd {
 
 template <bool EXACT, int NPP, int TPP>
@@ -47,7 +51,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
         if (TPP > 1) __syncthreads();
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-    energy2<EXACT, NPP, TPP, false>(L, G, S, T, sub, e0, e1, a0, a1);
+    energy2<EXACT, NPP, TPP, false, VD_SCORE_SPLIT != 0>(L, G, S, T, sub, e0, e1, a0, a1);
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
