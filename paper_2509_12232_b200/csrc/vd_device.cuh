@@ -492,11 +492,11 @@ __device__ __forceinline__ float atom_term(const GridView &G, const float *__res
  * resident warps, the GA kernel (register-bound by its other stages anyway) pipelines. */
 template <bool EXACT, int NPP, int TPP, bool PIPE>
 __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, const float2 *S,
-                                       int sub, double &e0, double &e1)
+                                       int sub, int ia, int ib, double &e0, double &e1)
 {
     if (G.yz != nullptr && !EXACT) {
-        const int n = L.n_atoms;
-        int i = sub;
+        const int n = ib;
+        int i = ia + sub;
         if (i >= n) return;
         Gather c0, c1;
         {
@@ -538,7 +538,7 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
     const float *emap = G.maps + G.mstride * L.elec_map;
     const float *dmap = G.maps + G.mstride * L.desolv_map;
 #pragma unroll 2
-    for (int i = sub; i < L.n_atoms; i += TPP) {
+    for (int i = ia + sub; i < ib; i += TPP) {
         const float4 a = L.atom[i];
         const float2 a2 = L.atom2[i];
         const float *tmap = G.maps + G.mstride * __float_as_int(a2.y);
@@ -654,18 +654,23 @@ __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, con
  * lanes of a warp process the same pair.  Per pair that is 3 LDS.64 of the j atom instead
  * of 6: the shared-memory wavefronts of this loop were the largest user of the L1 data
  * pipe the grid gathers also need. */
+#ifndef VD_SPLIT_R
+#define VD_SPLIT_R 21.7f   /* cost of one atom's gathers in pair-term units (cfg1 sweep) */
+#endif
+constexpr float kSplitR = VD_SPLIT_R;
 #ifndef VD_ROLE_NI8
 #define VD_ROLE_NI8 4   /* gather subs per 8 subs in the role-split energy stage */
 #endif
 #ifndef VD_INTRA_ROWS
 #define VD_INTRA_ROWS 1
 #endif
-template <int NPP, int TPP, bool HB, bool CUT>
+template <int NPP, bool HB, bool CUT>
 __device__ __forceinline__ float2 rows_fast(const float2 *S, int kb, int ke, const float4 *tc,
-                                            const int2 *toff, int sub, float cut2)
+                                            const int2 *toff, unsigned c0, unsigned c1, float cut2)
 {
+    /* this sub's part [c0, c1) (16.16 fractions) of the range: contiguous, no overlap */
     const int n = ke - kb;
-    const int k0 = kb + (n * sub) / TPP, k1 = kb + (n * (sub + 1)) / TPP;
+    const int k0 = kb + (int)(((unsigned)n * c0) >> 16), k1 = kb + (int)(((unsigned)n * c1) >> 16);
     float2 acc = f2(0.0f), xi = f2(0.0f), yi = f2(0.0f), zi = f2(0.0f);
     int ci = -1;
 #pragma unroll kFlatUnroll
@@ -736,8 +741,13 @@ __device__ __forceinline__ void exact_pair(const float2 *S, const PairTile &T, i
 /* intra of both poses over this sub's share of the pairs (all CTA threads must call) */
 template <bool EXACT, int NPP, int TPP>
 __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const PairTile &T,
-                                       int sub, double &a0, double &a1)
+                                       int sub, double &a0, double &a1,
+                                       unsigned w0 = ~0u, unsigned w1 = ~0u)
 {
+    if (w0 == ~0u) {  /* default: equal parts per sub */
+        w0 = ((unsigned)sub << 16) / TPP;
+        w1 = ((unsigned)(sub + 1) << 16) / TPP;
+    }
     const int n = L.n_pairs;
     if (n == 0) return;
     if (EXACT) {
@@ -810,10 +820,10 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
                 const int kb = c0, ke = min(tcnt, c0 + kTile);
                 const int kh = min(ke, max(kb, L.n_nohb - t0));  /* 12-6 | 12-10 boundary */
 #if VD_INTRA_ROWS
-                float2 part = cut ? rows_fast<NPP, TPP, false, true>(S, kb, kh, T.coef, T.off, sub, L.cut2)
-                                  : rows_fast<NPP, TPP, false, false>(S, kb, kh, T.coef, T.off, sub, L.cut2);
-                part = fadd2(part, cut ? rows_fast<NPP, TPP, true, true>(S, kh, ke, T.coef, T.off, sub, L.cut2)
-                                       : rows_fast<NPP, TPP, true, false>(S, kh, ke, T.coef, T.off, sub, L.cut2));
+                float2 part = cut ? rows_fast<NPP, false, true>(S, kb, kh, T.coef, T.off, w0, w1, L.cut2)
+                                  : rows_fast<NPP, false, false>(S, kb, kh, T.coef, T.off, w0, w1, L.cut2);
+                part = fadd2(part, cut ? rows_fast<NPP, true, true>(S, kh, ke, T.coef, T.off, w0, w1, L.cut2)
+                                       : rows_fast<NPP, true, false>(S, kh, ke, T.coef, T.off, w0, w1, L.cut2));
 #else
                 float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, kh, T.coef, T.off, sub, L.cut2)
                                   : flat_fast<NPP, TPP, false, false>(S, kb, kh, T.coef, T.off, sub, L.cut2);
@@ -841,14 +851,31 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
        CTA barriers).  cfg1: 1.603 vs 1.683 ms (NI = 2 of 4); NI = 1 or 3 of 4: 2.23 / 1.76 ms.
        The GA does not split (7,022 vs 8,621 ligands/s): it pipelines its gathers instead. */
     constexpr int NI = TPP * VD_ROLE_NI8 / 8 > 0 ? TPP * VD_ROLE_NI8 / 8 : 1;
+    constexpr int NA = TPP - NI > 0 ? TPP - NI : 1;
     if (SPLIT && !EXACT && TPP >= 4 && NI < TPP && T.resident) {
-        if (sub < NI)
-            inter2<EXACT, NPP, NI, PIPE>(L, G, S, sub, e0, e1);
-        else
-            intra2<EXACT, NPP, (TPP - NI > 0 ? TPP - NI : 1)>(L, S, T, sub - NI, a0, a1);
+        /* balance the two roles with the measured cost ratio of one atom's gathers to one
+           pair (kSplitR): the pair subs also take the last xa atoms, or the gather subs the
+           last px share of the pairs.  cfg1 (40 atoms, 608 pairs): xa = 6; swept 0/2/4/6/8/10/12
+           atoms: 1.597/1.577/1.560/1.545/1.550/1.558/1.567 ms; giving the gather subs 10% of
+           the pairs instead: 1.675 ms. */
+        const int n = L.n_atoms, np = L.n_pairs;
+        const float ex = (float)n - (float)np * (1.0f / kSplitR);
+        const int xa = ex > 0.f ? min(n, (int)(0.5f * ex + 0.5f)) : 0;
+        const unsigned px = ex < 0.f ? (unsigned)(-ex * kSplitR / (2.0f * (float)np) * 65536.0f) : 0u;
+        const int acut = n - xa;
+        if (sub < NI) {
+            inter2<EXACT, NPP, NI, PIPE>(L, G, S, sub, 0, acut, e0, e1);
+            if (px) intra2<EXACT, NPP, NA>(L, S, T, sub, a0, a1, 65536u - px + sub * px / NI,
+                                           65536u - px + (sub + 1) * px / NI);
+        } else {
+            const int s = sub - NI;
+            intra2<EXACT, NPP, NA>(L, S, T, s, a0, a1, s * (65536u - px) / NA,
+                                   (s + 1) * (65536u - px) / NA);
+            if (acut < n) inter2<EXACT, NPP, NA, PIPE>(L, G, S, s, acut, n, e0, e1);
+        }
         return;
     }
-    inter2<EXACT, NPP, TPP, PIPE>(L, G, S, sub, e0, e1);
+    inter2<EXACT, NPP, TPP, PIPE>(L, G, S, sub, 0, L.n_atoms, e0, e1);
     intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }
 

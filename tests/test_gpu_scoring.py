@@ -280,3 +280,23 @@ def test_fast_mode_every_launch_shape(cuda, tpp, monkeypatch):
     b = CudaBackend(mode="fast", device=0)
     e, a, t = b.score_population_arrays(c["genes"], c["ctx"])
     assert fx.within_tol(t, c["total"]).all()
+
+
+@pytest.mark.parametrize("heavy", [16, 30, 40, 48])
+def test_fast_mode_role_split_balance(cuda, heavy):
+    """The score kernel's role split hands the last atoms to the pair subs (few pairs per
+    atom, e.g. 21 atoms / 129 pairs) or the last pairs to the gather subs (many pairs per
+    atom, e.g. 64 atoms / 1,750 resident pairs).  Both hand-overs agree with the oracle."""
+    from paper_2509_12232_b200 import synth
+    from paper_2509_12232_b200.context import prepare_context
+
+    c = fx.pop_case("cfg1")
+    topo = synth.make_ligand(100 + heavy, heavy, heavy // 3, 6)
+    ctx = prepare_context(topo, c["grid"])
+    spec = c["grid"].spec
+    genes = synth.random_genes(heavy, 4096, ctx.n_torsions, spec.origin, spec.upper)
+    e, a, t = cuda["fast"].score_population_arrays(genes, ctx)
+    we, wa, wt = oracle.dock_population(oracle.Ligand(ctx), genes, n_threads=0)
+    assert fx.within_tol(t, wt).all()
+    assert fx.within_tol(e, we).all()
+    assert fx.within_tol(a, wa).all()
