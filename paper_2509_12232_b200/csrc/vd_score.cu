@@ -13,6 +13,11 @@
 
 #include "vd_internal.h"
 
+#ifndef VD_SCORE_PIPE
+#define VD_SCORE_PIPE 0    /* software-pipelined gathers (see inter2) */
+#endif
+/* (no min-blocks argument: __launch_bounds__(256, 1) lets ptxas take 140 registers instead
+   of 98, which halves the resident CTAs: 2.21 vs 1.56 ms on cfg1) */
 #ifndef VD_SCORE_SPLIT
 #define VD_SCORE_SPLIT 1   /* role-split energy stage (see energy2) */
 #endif
@@ -51,7 +56,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
         if (TPP > 1) __syncthreads();
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-    energy2<EXACT, NPP, TPP, false, VD_SCORE_SPLIT != 0>(L, G, S, T, sub, e0, e1, a0, a1);
+    energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0>(L, G, S, T, sub, e0, e1, a0, a1);
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
