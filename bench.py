@@ -337,6 +337,10 @@ def run_ours(args):
             rec = br.make_record(s["workload"], "cuda", [s["ms"]], s["ligands"], fl, by,
                                  threads=world)
             br.emit_csv([rec], args.csv)
+    if not args.no_extra:
+        line["stress"] = stress_leg(args, rank, world, dist, dev)
+        if rank == 0:
+            line["single_dock"] = single_dock_leg(args, dev)
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(ctx, genes_h, args.cpu_seconds)
     if rank == 0:
@@ -409,6 +413,101 @@ def screening_leg(args, rank, world, dist, dev):
             "timing": "CUDA events around vd_dock_batch (one persistent GA launch per atom-count bucket, buckets concurrent), max over ranks",
             **({"cpu_baseline": cpu} if cpu else {}),
             "_modeled": modeled}
+
+
+def stress_leg(args, rank, world, dist, dev):
+    """cfg4 (BASELINE configs[4]): 2,000 ligands of 128 atoms / 32 torsions, 126^3 x 10 maps
+    from an 8,000-atom receptor (built on the device), GA pop 512 x 300 generations, ligands
+    split by index over ranks; ligands/s device-timed, max over ranks."""
+    import torch
+
+    from paper_2509_12232_b200 import gridmaps, hostprep, synth
+    from paper_2509_12232_b200.backend import CudaBackend
+    from paper_2509_12232_b200.ga import GaConfig, _run
+    from paper_2509_12232_b200.screening import shard_range
+
+    spec = synth.config_grid_spec(4)
+    t0 = time.perf_counter()
+    gset = gridmaps.build_grid_maps(synth.config_protein(4), spec, synth.CONFIGS[4].probe_types)
+    grid_s = time.perf_counter() - t0
+    n = args.stress_ligands
+    lo, hi = shard_range(n, rank, world)
+    batch = hostprep.TopologyBatch.synth(4, lo, hi - lo)
+    arrays = hostprep.prepare_batch(batch, list(gset.maps))
+    b = CudaBackend(mode="fast", device=dev.index)
+    grid = b._grid_for_set(gset)
+    lset = hostprep.ligand_set(arrays)
+    gmax = 7 + int(batch.n_torsions.max())
+    bounds = (spec.origin, spec.upper)
+    ga = GaConfig(population_size=512, generations=300, translation_bounds=bounds)
+    _run(grid, lset, 0, min(4, hi - lo), GaConfig(population_size=512, generations=1,
+         translation_bounds=bounds), 0, lo, b._mode(), gmax, trace=False)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    _run(grid, lset, 0, hi - lo, ga, 0, lo, b._mode(), gmax, trace=False)
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    t = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    npairs = float(arrays["pair_start"][-1]) / max(1, hi - lo)
+    return {"metric": "ligands docked/sec", "value": n / t, "unit": "ligands/s",
+            "pose_evals_per_s": n * 512 * 301 / t, "ligands": n, "ms": 1e3 * t,
+            "workload": "cfg4-stress" if n == 2000 else f"cfg4-distribution x{n}",
+            "ligand": f"{int(batch.n_atoms.max())} atoms, {int(batch.n_torsions.max())} torsions, "
+                      f"{npairs:.0f} pairs on average",
+            "ga": "pop 512 x 300 generations", "grid": "126^3 x 10 maps, 8000-atom receptor",
+            "grid_build_s": round(grid_s, 3),
+            "timing": "CUDA events around vd_dock_batch, max over ranks"}
+
+
+def single_dock_leg(args, dev):
+    """cfg0 (BASELINE configs[0]): one 32-atom / 6-torsion ligand, 48^3 maps from a 2,000-atom
+    receptor, GA pop 100 x 50, seed 0, through the public ga.dock (context preparation
+    included), 10 runs dropping the 3 slowest (vd/bench.py:97-98); the restated GA on one host
+    core beside it."""
+    import torch
+
+    from oracle import oracle
+    from paper_2509_12232_b200 import gridmaps, synth
+    from paper_2509_12232_b200.backend import CudaBackend
+    from paper_2509_12232_b200.context import prepare_context
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    spec = synth.config_grid_spec(0)
+    gset = gridmaps.build_grid_maps(synth.config_protein(0), spec, synth.CONFIGS[0].probe_types)
+    topo = synth.config_ligand(0, 0)
+    cfg = GaConfig(population_size=100, generations=50, seed=0)
+    b = CudaBackend(mode="fast", device=dev.index)
+    dock(topo, gset, cfg, backend=b)
+    ts = []
+    for _ in range(10):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        r = dock(topo, gset, cfg, backend=b)
+        ts.append(time.perf_counter() - t0)
+    gpu_s = float(np.mean(sorted(ts)[:7]))
+    out = {"metric": "seconds per dock", "value": gpu_s, "unit": "s", "higher_is_better": False,
+           "workload": "cfg0-single-dock", "best_total": float(r.best_score.total),
+           "timing": "wall clock around ga.dock (host context prep + one GA launch + copies), "
+                     "mean of the 7 fastest of 10"}
+    if not args.no_cpu:
+        lig = oracle.Ligand(prepare_context(topo, gset))
+        params = oracle.ga_params(cfg, spec.origin, spec.upper)
+        cs = []
+        for _ in range(10):
+            t0 = time.perf_counter()
+            oracle.dock(lig, params, 0, 0)
+            cs.append(time.perf_counter() - t0)
+        out["cpu_baseline"] = {"value": float(np.mean(sorted(cs)[:7])), "unit": "s", "cores": 1,
+                               "kind": "port", "sample": "the same dock (restated GA, "
+                               "oracle/vd_ga_oracle.c) on one host core, 7 fastest of 10"}
+    return out
 
 
 def cpu_screen_baseline(gset, batch, ga, index_base, seconds=10.0):
@@ -522,6 +621,10 @@ def main():
     ap.add_argument("--csv", default=None, help="also write a BenchRecord CSV row (vd/bench.py schema)")
     ap.add_argument("--screen-ligands", type=int, default=10000,
                     help="cfg2 ligands for the ligands/s leg (0 disables)")
+    ap.add_argument("--stress-ligands", type=int, default=2000,
+                    help="cfg4 ligands for the stress leg")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the cfg4 stress and cfg0 single-dock legs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -3,7 +3,7 @@
 #   tools/ab_bench.sh base minb3 ...   ("base" = the in-tree library)
 for v in "$@"; do
   lib=""; [ "$v" != base ] && lib=tmp_ab/$v/libvdb200.so
-  VD_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu ${AB_ARGS:-} > gpurun_out/ab_$v.log 2>&1
+  VD_LIB=$lib timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu --no-extra ${AB_ARGS:-} > gpurun_out/ab_$v.log 2>&1
   python - "$v" <<'PY'
 import json, sys
 v = sys.argv[1]
