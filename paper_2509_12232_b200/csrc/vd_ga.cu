@@ -159,6 +159,9 @@ struct GaLayout {
 #ifndef VD_GA_MINB
 #define VD_GA_MINB 1
 #endif
+#ifndef VD_GA_SPLIT
+#define VD_GA_SPLIT 0  /* role-split energy stage (see energy2; slower for the GA, measured) */
+#endif
 #ifndef VD_GA_PIPE
 #define VD_GA_PIPE 1   /* software-pipelined grid gathers (see inter2) */
 #endif
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridVie
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, false>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
