@@ -88,11 +88,14 @@ def gather_records(rec: np.ndarray, n_total: int, dist=None, device=None) -> np.
 
     world = dist.get_world_size()
     per = math.ceil(n_total / world)
-    width = rec.shape[1]
-    buf = np.zeros((per, width), np.float64)
-    buf[: rec.shape[0]] = rec
     backend = dist.get_backend()
     dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+    # ranks may hold different max torsion counts (gene widths): agree on the widest
+    w = torch.tensor([rec.shape[1]], dtype=torch.int64, device=dev)
+    dist.all_reduce(w, op=dist.ReduceOp.MAX)
+    width = int(w.item())
+    buf = np.zeros((per, width), np.float64)
+    buf[: rec.shape[0], : rec.shape[1]] = rec
     t = torch.from_numpy(buf).to(dev)
     out = torch.empty((world * per, width), dtype=torch.float64, device=dev)
     dist.all_gather_into_tensor(out, t)

@@ -37,7 +37,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _gather_worker(rank, world, port, n, q):
+def _gather_worker(rank, world, port, n, q, widths=(4, 4)):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -46,7 +46,7 @@ def _gather_worker(rank, world, port, n, q):
     m = hi - lo
     idx = np.arange(lo, hi, dtype=np.float64)
     rec = pack_records(idx.astype(np.float32), idx * 2, idx * 3, np.full(m, 7),
-                       np.tile(idx[:, None], (1, 4)), np.ones(m))
+                       np.tile(idx[:, None], (1, widths[rank])), np.ones(m))
     out = gather_records(rec, n, dist)
     q.put((rank, out))
     dist.destroy_process_group()
@@ -72,6 +72,31 @@ def test_gather_records_gloo_world2():
         np.testing.assert_array_equal(out[:, 1], 2.0 * np.arange(n))
         np.testing.assert_array_equal(out[:, 4], np.ones(n))
         np.testing.assert_array_equal(out[:, REC_HEAD], np.arange(n))
+
+
+def test_gather_records_gloo_world2_ragged_gene_widths():
+    """Ranks whose shards hold different max torsion counts (gene widths 7+3 and 7+9) agree
+    on the widest record; the narrower rank's genes are zero-padded."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    n, world, port = 9, 2, _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, n, q, (3, 9)))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    lo1, _ = shard_range(n, 1, world)
+    for r in range(world):
+        out = got[r]
+        assert out.shape == (n, REC_HEAD + 9)
+        np.testing.assert_array_equal(out[:, 0], np.arange(n, dtype=np.float32))
+        np.testing.assert_array_equal(out[:lo1, REC_HEAD + 3:], 0.0)
+        np.testing.assert_array_equal(out[lo1:, REC_HEAD + 8], np.arange(lo1, n))
 
 
 # --- reference registry plumbing -------------------------------------------------
