@@ -173,9 +173,13 @@ vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)
     return v;
 }
 
+/* Host-buffer pipeline: copy-in, kernel and copy-out each on their own stream, chained by
+ * events over a ring of kRing staging slots, so the H2D engine (the e2e bound: 120 B of f64
+ * genes per pose at ~54 GB/s) never waits for a kernel or a copy-out. */
+constexpr int kRing = 3;
 struct Pipe {
-    cudaStream_t s[2];
-    cudaEvent_t start, done[2];
+    cudaStream_t h, k, d;
+    cudaEvent_t start, eh[kRing], ek[kRing], ed[kRing];
 };
 
 static Pipe *pipe_for_device()
@@ -186,9 +190,13 @@ static Pipe *pipe_for_device()
     auto it = pipes.find(dev);
     if (it != pipes.end()) return &it->second;
     Pipe p;
-    for (int k = 0; k < 2; ++k) {
-        cudaStreamCreateWithFlags(&p.s[k], cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&p.done[k], cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&p.h, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p.k, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&p.d, cudaStreamNonBlocking);
+    for (int r = 0; r < kRing; ++r) {
+        cudaEventCreateWithFlags(&p.eh[r], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&p.ek[r], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&p.ed[r], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
     return &(pipes[dev] = p);
@@ -473,59 +481,89 @@ static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const vo
                                total, cs));
         return 0;
     }
-    /* chunked two-stream pipeline through device staging buffers */
+    /* chunked pipeline through a ring of device staging slots (see Pipe).  Chunks of CH
+       poses, the last CH split in halves and quarters so the final kernel + copy-out that
+       trail the last copy-in are short. */
     vdi::Pipe *pp = vdi::pipe_for_device();
     static const int64_t chunk_env = getenv("VD_CHUNK") ? atoll(getenv("VD_CHUNK")) : 0;
     const int64_t CH = std::min<int64_t>(P, chunk_env > 0 ? chunk_env : (1 << 17));
-    char *d_in[2] = {nullptr, nullptr};
-    double *d_e[2] = {nullptr, nullptr}, *d_a[2] = {nullptr, nullptr};
-    float *d_t[2] = {nullptr, nullptr};
+    std::vector<std::pair<int64_t, int64_t>> chunks;  /* (offset, count) */
+    {
+        int64_t off = 0;
+        while (P - off > CH) {
+            chunks.push_back({off, CH});
+            off += CH;
+        }
+        int64_t rest = P - off, piece = std::max<int64_t>(CH / 2, 1);
+        while (rest > 0) {
+            const int64_t n = rest > piece && piece >= 4096 ? piece : rest;
+            chunks.push_back({off, n});
+            off += n;
+            rest -= n;
+            piece /= 2;
+        }
+    }
+    char *d_in[vdi::kRing] = {};
+    double *d_e[vdi::kRing] = {}, *d_a[vdi::kRing] = {};
+    float *d_t[vdi::kRing] = {};
     VD_CK(cudaEventRecord(pp->start, cs));
+    VD_CK(cudaStreamWaitEvent(pp->h, pp->start, 0));
+    VD_CK(cudaStreamWaitEvent(pp->k, pp->start, 0));
+    VD_CK(cudaStreamWaitEvent(pp->d, pp->start, 0));
     int rc = 0;
-    for (int k = 0; k < 2 && rc == 0; ++k) {
-        cudaStream_t st = pp->s[k];
-        if (!vdi::check(cudaStreamWaitEvent(st, pp->start, 0), "wait") ||
-            (!in_dev && !vdi::check(cudaMallocAsync((void **)&d_in[k], CH * in_row, st), "alloc in")) ||
-            (!oe && !vdi::check(cudaMallocAsync((void **)&d_e[k], CH * sizeof(double), st), "alloc e")) ||
-            (!oa && !vdi::check(cudaMallocAsync((void **)&d_a[k], CH * sizeof(double), st), "alloc a")) ||
-            (total && !ot && !vdi::check(cudaMallocAsync((void **)&d_t[k], CH * sizeof(float), st), "alloc t")))
+    for (int r = 0; r < vdi::kRing && rc == 0; ++r) {
+        if ((!in_dev && !vdi::check(cudaMallocAsync((void **)&d_in[r], CH * in_row, pp->h), "alloc in")) ||
+            (!oe && !vdi::check(cudaMallocAsync((void **)&d_e[r], CH * sizeof(double), pp->k), "alloc e")) ||
+            (!oa && !vdi::check(cudaMallocAsync((void **)&d_a[r], CH * sizeof(double), pp->k), "alloc a")) ||
+            (total && !ot && !vdi::check(cudaMallocAsync((void **)&d_t[r], CH * sizeof(float), pp->k), "alloc t")))
             rc = -1;
     }
-    for (int64_t off = 0, c = 0; off < P && rc == 0; off += CH, ++c) {
-        const int k = (int)(c & 1);
-        cudaStream_t st = pp->s[k];
-        const int64_t n = std::min(CH, P - off);
+    /* the kernel stream's output slots must exist before the first kernel: order k after h */
+    if (rc == 0 && !vdi::check(cudaEventRecord(pp->eh[0], pp->h), "event") ) rc = -1;
+    if (rc == 0 && !vdi::check(cudaStreamWaitEvent(pp->k, pp->eh[0], 0), "wait")) rc = -1;
+    for (size_t c = 0; c < chunks.size() && rc == 0; ++c) {
+        const int r = (int)(c % vdi::kRing);
+        const int64_t off = chunks[c].first, n = chunks[c].second;
         const char *src_in = (const char *)in + off * in_row;
         const void *kin = src_in;
         if (!in_dev) {
-            if (!vdi::check(cudaMemcpyAsync(d_in[k], src_in, n * in_row, cudaMemcpyHostToDevice, st), "H2D")) { rc = -1; break; }
-            kin = d_in[k];
+            /* slot r's previous kernel (chunk c - kRing) has read its input */
+            if (!vdi::check(cudaStreamWaitEvent(pp->h, pp->ek[r], 0), "wait k") ||
+                !vdi::check(cudaMemcpyAsync(d_in[r], src_in, n * in_row, cudaMemcpyHostToDevice, pp->h), "H2D") ||
+                !vdi::check(cudaEventRecord(pp->eh[r], pp->h), "event h") ||
+                !vdi::check(cudaStreamWaitEvent(pp->k, pp->eh[r], 0), "wait h")) { rc = -1; break; }
+            kin = d_in[r];
         }
-        double *ke = oe ? inter + off : d_e[k];
-        double *ka = oa ? intra + off : d_a[k];
-        float *kt = total ? (ot ? total + off : d_t[k]) : nullptr;
-        if (!vdi::check(vd::launch_score(mode, src, G, L, in_is_genes ? (const double *)kin : nullptr,
-                                         in_is_genes ? nullptr : (const float *)kin, n, ngenes, ke, ka, kt, st),
-                        "score kernel")) { rc = -1; break; }
-        if ((!oe && !vdi::check(cudaMemcpyAsync(inter + off, ke, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H e")) ||
-            (!oa && !vdi::check(cudaMemcpyAsync(intra + off, ka, n * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H a")) ||
-            (total && !ot && !vdi::check(cudaMemcpyAsync(total + off, kt, n * sizeof(float), cudaMemcpyDeviceToHost, st), "D2H t")))
-            rc = -1;
+        double *ke = oe ? inter + off : d_e[r];
+        double *ka = oa ? intra + off : d_a[r];
+        float *kt = total ? (ot ? total + off : d_t[r]) : nullptr;
+        /* slot r's previous copy-out (chunk c - kRing) has drained its outputs */
+        if (!vdi::check(cudaStreamWaitEvent(pp->k, pp->ed[r], 0), "wait d") ||
+            !vdi::check(vd::launch_score(mode, src, G, L, in_is_genes ? (const double *)kin : nullptr,
+                                         in_is_genes ? nullptr : (const float *)kin, n, ngenes, ke, ka, kt, pp->k),
+                        "score kernel") ||
+            !vdi::check(cudaEventRecord(pp->ek[r], pp->k), "event k") ||
+            !vdi::check(cudaStreamWaitEvent(pp->d, pp->ek[r], 0), "wait k")) { rc = -1; break; }
+        if ((!oe && !vdi::check(cudaMemcpyAsync(inter + off, ke, n * sizeof(double), cudaMemcpyDeviceToHost, pp->d), "D2H e")) ||
+            (!oa && !vdi::check(cudaMemcpyAsync(intra + off, ka, n * sizeof(double), cudaMemcpyDeviceToHost, pp->d), "D2H a")) ||
+            (total && !ot && !vdi::check(cudaMemcpyAsync(total + off, kt, n * sizeof(float), cudaMemcpyDeviceToHost, pp->d), "D2H t")) ||
+            !vdi::check(cudaEventRecord(pp->ed[r], pp->d), "event d")) { rc = -1; break; }
     }
-    for (int k = 0; k < 2; ++k) {
-        cudaStream_t st = pp->s[k];
-        if (d_in[k]) cudaFreeAsync(d_in[k], st);
-        if (d_e[k]) cudaFreeAsync(d_e[k], st);
-        if (d_a[k]) cudaFreeAsync(d_a[k], st);
-        if (d_t[k]) cudaFreeAsync(d_t[k], st);
-        cudaEventRecord(pp->done[k], st);
-        cudaStreamWaitEvent(cs, pp->done[k], 0);
+    /* join: the slots are freed on the copy-out stream once everything has drained */
+    cudaEventRecord(pp->eh[0], pp->h);
+    cudaStreamWaitEvent(pp->d, pp->eh[0], 0);
+    cudaEventRecord(pp->ek[0], pp->k);
+    cudaStreamWaitEvent(pp->d, pp->ek[0], 0);
+    for (int r = 0; r < vdi::kRing; ++r) {
+        if (d_in[r]) cudaFreeAsync(d_in[r], pp->d);
+        if (d_e[r]) cudaFreeAsync(d_e[r], pp->d);
+        if (d_a[r]) cudaFreeAsync(d_a[r], pp->d);
+        if (d_t[r]) cudaFreeAsync(d_t[r], pp->d);
     }
+    cudaEventRecord(pp->ed[0], pp->d);
+    cudaStreamWaitEvent(cs, pp->ed[0], 0);
     if (rc) return rc;
-    if (!(oe && oa && ot)) {
-        VD_CK(cudaStreamSynchronize(pp->s[0]));
-        VD_CK(cudaStreamSynchronize(pp->s[1]));
-    }
+    if (!(oe && oa && ot)) VD_CK(cudaStreamSynchronize(pp->d));
     return 0;
 }
 
