@@ -180,6 +180,12 @@ constexpr int kRing = 3;
 struct Pipe {
     cudaStream_t h, k, d;
     cudaEvent_t start, eh[kRing], ek[kRing], ed[kRing];
+    /* staging slots, kept between calls (grown on demand) */
+    char *in[kRing] = {};
+    double *e[kRing] = {}, *a[kRing] = {};
+    float *t[kRing] = {};
+    size_t in_cap = 0;
+    int64_t out_cap = 0;
 };
 
 static Pipe *pipe_for_device()
@@ -503,24 +509,43 @@ static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const vo
             piece /= 2;
         }
     }
-    char *d_in[vdi::kRing] = {};
-    double *d_e[vdi::kRing] = {}, *d_a[vdi::kRing] = {};
-    float *d_t[vdi::kRing] = {};
     VD_CK(cudaEventRecord(pp->start, cs));
     VD_CK(cudaStreamWaitEvent(pp->h, pp->start, 0));
     VD_CK(cudaStreamWaitEvent(pp->k, pp->start, 0));
     VD_CK(cudaStreamWaitEvent(pp->d, pp->start, 0));
-    int rc = 0;
-    for (int r = 0; r < vdi::kRing && rc == 0; ++r) {
-        if ((!in_dev && !vdi::check(cudaMallocAsync((void **)&d_in[r], CH * in_row, pp->h), "alloc in")) ||
-            (!oe && !vdi::check(cudaMallocAsync((void **)&d_e[r], CH * sizeof(double), pp->k), "alloc e")) ||
-            (!oa && !vdi::check(cudaMallocAsync((void **)&d_a[r], CH * sizeof(double), pp->k), "alloc a")) ||
-            (total && !ot && !vdi::check(cudaMallocAsync((void **)&d_t[r], CH * sizeof(float), pp->k), "alloc t")))
-            rc = -1;
+    if ((!in_dev && (size_t)CH * in_row > pp->in_cap) || ((!oe || !oa || !ot) && CH > pp->out_cap)) {
+        /* grow the slots: drain whatever still uses the old ones */
+        VD_CK(cudaStreamSynchronize(pp->h));
+        VD_CK(cudaStreamSynchronize(pp->k));
+        VD_CK(cudaStreamSynchronize(pp->d));
+        if (!in_dev && (size_t)CH * in_row > pp->in_cap) {
+            for (int r = 0; r < vdi::kRing; ++r) {
+                cudaFree(pp->in[r]);
+                pp->in[r] = nullptr;
+            }
+            pp->in_cap = 0;
+            for (int r = 0; r < vdi::kRing; ++r) VD_CK(cudaMalloc((void **)&pp->in[r], CH * in_row));
+            pp->in_cap = (size_t)CH * in_row;
+        }
+        if ((!oe || !oa || !ot) && CH > pp->out_cap) {
+            for (int r = 0; r < vdi::kRing; ++r) {
+                cudaFree(pp->e[r]); cudaFree(pp->a[r]); cudaFree(pp->t[r]);
+                pp->e[r] = pp->a[r] = nullptr;
+                pp->t[r] = nullptr;
+            }
+            pp->out_cap = 0;
+            for (int r = 0; r < vdi::kRing; ++r) {
+                VD_CK(cudaMalloc((void **)&pp->e[r], CH * sizeof(double)));
+                VD_CK(cudaMalloc((void **)&pp->a[r], CH * sizeof(double)));
+                VD_CK(cudaMalloc((void **)&pp->t[r], CH * sizeof(float)));
+            }
+            pp->out_cap = CH;
+        }
     }
-    /* the kernel stream's output slots must exist before the first kernel: order k after h */
-    if (rc == 0 && !vdi::check(cudaEventRecord(pp->eh[0], pp->h), "event") ) rc = -1;
-    if (rc == 0 && !vdi::check(cudaStreamWaitEvent(pp->k, pp->eh[0], 0), "wait")) rc = -1;
+    char **d_in = pp->in;
+    double **d_e = pp->e, **d_a = pp->a;
+    float **d_t = pp->t;
+    int rc = 0;
     for (size_t c = 0; c < chunks.size() && rc == 0; ++c) {
         const int r = (int)(c % vdi::kRing);
         const int64_t off = chunks[c].first, n = chunks[c].second;
@@ -549,17 +574,11 @@ static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const vo
             (total && !ot && !vdi::check(cudaMemcpyAsync(total + off, kt, n * sizeof(float), cudaMemcpyDeviceToHost, pp->d), "D2H t")) ||
             !vdi::check(cudaEventRecord(pp->ed[r], pp->d), "event d")) { rc = -1; break; }
     }
-    /* join: the slots are freed on the copy-out stream once everything has drained */
+    /* join: the caller's stream waits for all three pipeline streams */
     cudaEventRecord(pp->eh[0], pp->h);
     cudaStreamWaitEvent(pp->d, pp->eh[0], 0);
     cudaEventRecord(pp->ek[0], pp->k);
     cudaStreamWaitEvent(pp->d, pp->ek[0], 0);
-    for (int r = 0; r < vdi::kRing; ++r) {
-        if (d_in[r]) cudaFreeAsync(d_in[r], pp->d);
-        if (d_e[r]) cudaFreeAsync(d_e[r], pp->d);
-        if (d_a[r]) cudaFreeAsync(d_a[r], pp->d);
-        if (d_t[r]) cudaFreeAsync(d_t[r], pp->d);
-    }
     cudaEventRecord(pp->ed[0], pp->d);
     cudaStreamWaitEvent(cs, pp->ed[0], 0);
     if (rc) return rc;

@@ -24,3 +24,11 @@ for name, g, o in (("dev", gd, od), ("pinned", pin.numpy(), outs_np), ("pageable
         torch.cuda.synchronize(); dt = time.perf_counter() - t0
         print(name, k, f"{dt*1e3:.2f} ms  {N/dt/1e6:.1f} M poses/s")
 t0 = time.perf_counter(); x = pin.cuda(non_blocking=False); torch.cuda.synchronize(); print("torch H2D 120MB", (time.perf_counter()-t0)*1e3, "ms")
+# fixed overhead vs size: slope = per-pose cost, intercept = per-call overhead
+for n in (1 << 14, 1 << 17, 1 << 18, 1 << 19, N):
+    g, o = pin.numpy()[:n], tuple(x[:n] for x in outs_np)
+    b.score_population_arrays(g, ctx, out=o)
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    for _ in range(10): b.score_population_arrays(g, ctx, out=o)
+    torch.cuda.synchronize(); dt = (time.perf_counter() - t0) / 10
+    print(f"P={n:8d} {dt*1e3:.3f} ms  H2D-bound {n*120/54e9*1e3:.3f} ms")
