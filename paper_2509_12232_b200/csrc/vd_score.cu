@@ -147,21 +147,40 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     auto k = score_kernel<EXACT, NPP, TPP>;
     /* the attribute / occupancy set-up below costs ~10 driver calls; a host-buffer batch
        launches once per pipeline chunk, so it is done once per (device, shared-memory size) */
-    struct Setup { int dev; unsigned bytes; int want, pct; };
+    /* (the function attributes are per kernel: the dynamic shared-memory limit only ever
+       grows, and the carveout is re-applied when another shape changed it) */
+    struct Setup { int dev; unsigned bytes; int pct; };
     static thread_local std::vector<Setup> done_setups;
+    static thread_local std::vector<std::pair<int, unsigned>> max_bytes;  /* (dev, limit set) */
+    static thread_local std::vector<std::pair<int, int>> last_pct;        /* (dev, carveout) */
     int cur_dev = 0;
     cudaGetDevice(&cur_dev);
+    unsigned *limit = nullptr;
+    int *carve = nullptr;
+    for (auto &m : max_bytes) if (m.first == cur_dev) limit = &m.second;
+    for (auto &c : last_pct) if (c.first == cur_dev) carve = &c.second;
+    if (!limit) { max_bytes.push_back({cur_dev, 0u}); limit = &max_bytes.back().second; }
+    if (!carve) { last_pct.push_back({cur_dev, -1}); carve = &last_pct.back().second; }
     const char *l1_env = getenv("VD_L1_KB"), *cv_env = getenv("VD_CARVEOUT");
     for (const Setup &x : done_setups)
         if (x.dev == cur_dev && x.bytes == lay.bytes && !l1_env && !cv_env) {
+            if (*carve != x.pct) {
+                cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, x.pct);
+                if (e != cudaSuccess) return e;
+                *carve = x.pct;
+            }
             const int64_t blocks = (P + 2 * NPP - 1) / (2 * NPP);
             k<<<(unsigned)blocks, NPP * TPP, lay.bytes, st>>>(G, L, genes, poses, P, ngenes, lay,
                                                                 inter, intra, total);
             ++vdi::g_launches;
             return cudaGetLastError();
         }
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
-    if (e != cudaSuccess) return e;
+    cudaError_t e = cudaSuccess;
+    if (lay.bytes > *limit) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
+        if (e != cudaSuccess) return e;
+        *limit = lay.bytes;
+    }
     /* Shared-memory carveout: as many CTAs per SM as fit while >= 32 KB of the 256 KB
        L1/shared array stays L1 for the grid gathers (an atom's corners share lines with
        its bonded neighbours').  cfg1 A/B, NPP 32: 1.77 ms at 3 CTAs (63 KB L1) vs 2.00 ms
@@ -178,9 +197,11 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     const int want = std::max(1, std::min(occ, fit));
     int pct = (int)((100LL * want * (lay.bytes + resv) + smem_sm - 1) / smem_sm);
     if (const char *cv = getenv("VD_CARVEOUT")) pct = atoi(cv);  /* tuning override */
-    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::min(100, pct));
+    pct = std::min(100, pct);
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     if (e != cudaSuccess) return e;
-    if (done_setups.size() < 64) done_setups.push_back({cur_dev, lay.bytes, want, pct});
+    *carve = pct;
+    if (done_setups.size() < 64) done_setups.push_back({cur_dev, lay.bytes, pct});
     const int64_t per_cta = 2 * NPP;
     const int64_t blocks = (P + per_cta - 1) / per_cta;
     if (getenv("VD_VERBOSE"))

@@ -300,3 +300,16 @@ def test_fast_mode_role_split_balance(cuda, heavy):
     assert fx.within_tol(t, wt).all()
     assert fx.within_tol(e, we).all()
     assert fx.within_tol(a, wa).all()
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+def test_alternating_ligand_sizes_reuse_launch_setup(cuda, mode):
+    """Launch set-up is cached per kernel shape; a larger ligand after a smaller one of the same
+    shape must still get its shared-memory limit (large -> small -> large, host buffers)."""
+    big, small = fx.pop_case("cfg1"), fx.pop_case("cfg0")
+    first = cuda[mode].score_population_arrays(big["genes"], big["ctx"])
+    cuda[mode].score_population_arrays(small["genes"], small["ctx"])
+    cuda[mode].score_many(small["poses"], small["ctx"])
+    again = cuda[mode].score_population_arrays(big["genes"], big["ctx"])
+    for x, y in zip(first, again):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
