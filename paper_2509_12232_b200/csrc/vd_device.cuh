@@ -116,12 +116,14 @@ constexpr float kMinR2 = 0.01f;
 __device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 /* Exact ops for the bit-exact pose stage, applied per component with scalar
- * IEEE intrinsics.  Packed f32x2 is NOT usable here: ptxas 12.9 fuses packed
+ * IEEE intrinsics.  Packed f32x2 is NOT usable naively: ptxas 12.9 fuses packed
  * multiply + add into FFMA2 (from __fmul2_rn/__fadd2_rn, from explicit
  * mul.rn/add.rn.f32x2 PTX, even under --fmad=false), which would break parity
- * with the reference's unfused float32 sequence.  (A packed variant that writes
- * adds as fma(x, one, y) with a run-time one -- which ptxas cannot fuse -- is
- * bit-exact too, but measured 2% slower on cfg1: 2.21 vs 2.16 ms.) */
+ * with the reference's unfused float32 sequence.  The packed variant below
+ * (xadd2/xsub2) writes every sum as fma(x, one, y) with a RUN-TIME one (a kernel
+ * argument): ptxas cannot fold a product into it, so it is bit-exact, and it
+ * halves the pose stage's FP32 instructions.  A compile-time 1.0f would be
+ * contracted again (caught by the fixture tests). */
 __device__ __forceinline__ float2 mul2(float2 a, float2 b)
 {
     return make_float2(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y));
@@ -134,6 +136,15 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b)
 {
     return make_float2(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y));
 }
+/* Exact packed ops (VD_POSE_PACKED): FMUL2 rounds each product; sums are written as
+ * fma(a, one, b) / fma(b, -one, a) with a run-time one, which ptxas cannot contract. */
+#ifndef VD_POSE_PACKED
+#define VD_POSE_PACKED 1   /* pose stage alone 0.441 -> 0.404 ms per 1M cfg1 poses; whole
+                              kernel 1.557 -> 1.543 ms; cfg2 screen +1.4% */
+#endif
+__device__ __forceinline__ float2 xmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 xadd2(float2 a, float2 b, float2 one) { return __ffma2_rn(a, one, b); }
+__device__ __forceinline__ float2 xsub2(float2 a, float2 b, float2 neg) { return __ffma2_rn(b, neg, a); }
 /* Contractible packed ops for the FAST energy stage. */
 __device__ __forceinline__ float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
@@ -206,8 +217,11 @@ __host__ __device__ inline int pose_scratch_floats(int n_tors) { return kPoseScr
 template <int NPP, int TPP>
 __device__ __forceinline__ void build_pose2(const LigView &L, const double *__restrict__ g0,
                                             const double *__restrict__ g1, float2 *S, int sub,
-                                            float *X)
+                                            float *X, float one)
 {
+#if VD_POSE_PACKED
+    const float2 ONE = f2(one), NEG = f2(-one);
+#endif
 #define VD_X(k) X[(k) * NPP]
     float2 M00, M01, M02, M10, M11, M12, M20, M21, M22, TX, TY, TZ;
     if (TPP == 1) {
@@ -244,9 +258,15 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
     for (int i = sub; i < L.n_atoms; i += TPP) {
         const float4 c = L.atom[i];
         const float2 cx = f2(c.x), cy = f2(c.y), cz = f2(c.z);
+#if VD_POSE_PACKED
+        VD_S2(i, 0) = xadd2(xadd2(xadd2(xmul2(M00, cx), xmul2(M01, cy), ONE), xmul2(M02, cz), ONE), TX, ONE);
+        VD_S2(i, 1) = xadd2(xadd2(xadd2(xmul2(M10, cx), xmul2(M11, cy), ONE), xmul2(M12, cz), ONE), TY, ONE);
+        VD_S2(i, 2) = xadd2(xadd2(xadd2(xmul2(M20, cx), xmul2(M21, cy), ONE), xmul2(M22, cz), ONE), TZ, ONE);
+#else
         VD_S2(i, 0) = add2(add2(add2(mul2(M00, cx), mul2(M01, cy)), mul2(M02, cz)), TX);
         VD_S2(i, 1) = add2(add2(add2(mul2(M10, cx), mul2(M11, cy)), mul2(M12, cz)), TY);
         VD_S2(i, 2) = add2(add2(add2(mul2(M20, cx), mul2(M21, cy)), mul2(M22, cz)), TZ);
+#endif
     }
     if (TPP > 1) __syncthreads();
     for (int t = 0; t < L.n_torsions; ++t) {
@@ -284,6 +304,18 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
 #pragma unroll 4
         for (int f = tr.z + sub; f < tr.w; f += TPP) {
             const int i = L.frag[f];
+#if VD_POSE_PACKED
+            const float2 vx = xsub2(VD_S2(i, 0), ox, NEG), vy = xsub2(VD_S2(i, 1), oy, NEG),
+                         vz = xsub2(VD_S2(i, 2), oz, NEG);
+            const float2 dot = xadd2(xadd2(xmul2(KX, vx), xmul2(KY, vy), ONE), xmul2(KZ, vz), ONE);
+            const float2 cxx = xsub2(xmul2(KY, vz), xmul2(KZ, vy), NEG);
+            const float2 cxy = xsub2(xmul2(KZ, vx), xmul2(KX, vz), NEG);
+            const float2 cxz = xsub2(xmul2(KX, vy), xmul2(KY, vx), NEG);
+            const float2 dw = xmul2(dot, OMC);
+            VD_S2(i, 0) = xadd2(xadd2(xadd2(xmul2(vx, C), xmul2(cxx, SN), ONE), xmul2(KX, dw), ONE), ox, ONE);
+            VD_S2(i, 1) = xadd2(xadd2(xadd2(xmul2(vy, C), xmul2(cxy, SN), ONE), xmul2(KY, dw), ONE), oy, ONE);
+            VD_S2(i, 2) = xadd2(xadd2(xadd2(xmul2(vz, C), xmul2(cxz, SN), ONE), xmul2(KZ, dw), ONE), oz, ONE);
+#else
             const float2 vx = sub2(VD_S2(i, 0), ox), vy = sub2(VD_S2(i, 1), oy),
                          vz = sub2(VD_S2(i, 2), oz);
             const float2 dot = add2(add2(mul2(KX, vx), mul2(KY, vy)), mul2(KZ, vz));
@@ -294,6 +326,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
             VD_S2(i, 0) = add2(add2(add2(mul2(vx, C), mul2(cxx, SN)), mul2(KX, dw)), ox);
             VD_S2(i, 1) = add2(add2(add2(mul2(vy, C), mul2(cxy, SN)), mul2(KY, dw)), oy);
             VD_S2(i, 2) = add2(add2(add2(mul2(vz, C), mul2(cxz, SN)), mul2(KZ, dw)), oz);
+#endif
         }
         if (TPP > 1) __syncthreads();
     }

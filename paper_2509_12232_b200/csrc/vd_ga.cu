@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridVie
                 const int i0 = b0 + 2 * pp, i1 = i0 + 1;
                 build_pose2<NPP, TPP>(L, cur + (size_t)min(i0, pop - 1) * G,
                                       cur + (size_t)min(i1, pop - 1) * G, S, sub,
-                                      reinterpret_cast<float *>(smem + lay.base.scratch) + pp);
+                                      reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0>(L, Gv, S, Tl, sub, e0, e1, a0, a1);

@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;  /* tail: duplicate, drop */
     if (genes) {
         build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
-                              reinterpret_cast<float *>(smem + lay.scratch) + pp);
+                              reinterpret_cast<float *>(smem + lay.scratch) + pp, G.one);
         if (TPP > 1) __syncthreads();
     } else {
         const int n = L.n_atoms;
@@ -57,7 +57,11 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
         if (TPP > 1) __syncthreads();
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
+#ifndef VD_TEST_STAGE
     energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0>(L, G, S, T, sub, e0, e1, a0, a1);
+#else  /* (timing only) the pose stage alone */
+    e0 = S[0].x; e1 = S[NPP].y;
+#endif
     reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
@@ -76,7 +80,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
 template <int NPP>
 __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__restrict__ genes,
                                                    int64_t P, int ngenes, SmemLayout lay,
-                                                   float *__restrict__ out)
+                                                   float one, float *__restrict__ out)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int pp = threadIdx.x;
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__r
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
     const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;
-    build_pose2<NPP, 1>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, 0, nullptr);
+    build_pose2<NPP, 1>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, 0, nullptr, one);
     const int n = L.n_atoms;
     for (int i = 0; i < n; ++i)
 #pragma unroll
@@ -249,7 +253,7 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
 #define VD_P(N)                                                                                   \
     if (npp == N) {                                                                               \
         e = cudaFuncSetAttribute(pose_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-        if (e == cudaSuccess) pose_kernel<N><<<(unsigned)blocks, N, smem, st>>>(L, genes, P, ngenes, lay, out); \
+        if (e == cudaSuccess) pose_kernel<N><<<(unsigned)blocks, N, smem, st>>>(L, genes, P, ngenes, lay, 1.0f /* run-time: see xadd2 */, out); \
     }
     VD_P(64) else VD_P(32) else VD_P(16) else return cudaErrorInvalidConfiguration;
 #undef VD_P
