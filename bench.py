@@ -42,7 +42,7 @@ WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
 # dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
 # committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
-TRAFFIC_BYTES = 165.56e6 + 20.80e6
+TRAFFIC_BYTES = 166.33e6 + 22.18e6
 TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,64,4>)"
 
 
@@ -105,7 +105,8 @@ def measure_peaks(grid_n=80, n_types=7):
     return out
 
 
-def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx):
+def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx,
+                   inbox_frac=None):
     """Both rooflines of SURVEY 8(d); the binding one (lower poses/s ceiling) is primary.
     Ridge = FP32 peak / L2 gather BW; the reference model's AI = fpp / (96 B * N)."""
     bpp = 96 * int(ctx.n_atoms)
@@ -124,6 +125,14 @@ def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx
                   "peak_source": "measured live: " + peaks["l2_gather_src"]
                                  + " (tools/peaks.cu), best of 3",
                   "peak_8b_random_gbs": peaks["l2_gather_8b_gbs"],
+                  "inbox_atom_fraction": inbox_frac,
+                  "achieved_inbox_only": (gather_bps * inbox_frac / 1e9
+                                          if inbox_frac is not None else None),
+                  "frac_inbox_only": (gather_bps * inbox_frac / 1e9 / l2
+                                      if inbox_frac is not None else None),
+                  "note": "achieved counts 96 B for every atom (the reference's model, "
+                          "vd/bench.py:166-171); out-of-box atoms issue no gathers, so the "
+                          "bytes actually gathered are the in-box-only figure",
                   "ceiling_poses_per_s": l2 * 1e9 / bpp}
         out["l2_gather"] = gather
         out["ridge_flop_per_byte"] = fp32_peak * 1e3 / l2
@@ -304,6 +313,12 @@ def run_ours(args):
     peak_src = ("measured live on this GPU: packed-FFMA2 microbenchmark (tools/peaks.cu), "
                 "best of 3" if peaks else "spec-derived 2*128 lanes*148 SMs*1.965 GHz")
     gather_bps = 96 * ctx.n_atoms * N_POSES / (t_loc / args.steps)
+    # share of atoms inside the grid box (the kernel gathers only for those; the reference's
+    # model counts every atom), from the device pose path on a sample of the genes
+    smp = b.pose_population(genes_h[:8192], ctx)
+    lo_b, hi_b = np.asarray(ctx.box_lo, np.float32), np.asarray(ctx.box_hi, np.float32)
+    inb = np.all((smp >= lo_b[None, :, None]) & (smp <= hi_b[None, :, None]), axis=1)
+    inbox_frac = float(inb.mean())
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -320,7 +335,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(genes_h.nbytes),
                 "d2h_bytes_per_step": int(N_POSES * (8 + 8 + 4)),
                 "path": "CudaBackend.score_population_arrays (pinned numpy in/out)"},
-        "roofline": roofline_block(achieved, peak, peak_src, gather_bps, peaks, fpp, ctx),
+        "roofline": roofline_block(achieved, peak, peak_src, gather_bps, peaks, fpp, ctx,
+                                   inbox_frac),
         "gpu_launches": int(launches),
         "parity_sample_ok": parity_ok,
         "clocks": clk.summary(),
