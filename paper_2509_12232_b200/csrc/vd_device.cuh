@@ -735,7 +735,7 @@ __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, con
  * of 6: the shared-memory wavefronts of this loop were the largest user of the L1 data
  * pipe the grid gathers also need. */
 #ifndef VD_SPLIT_R
-#define VD_SPLIT_R 21.7f   /* cost of one atom's gathers in pair-term units (cfg1 sweep) */
+#define VD_SPLIT_R 26.0f   /* cost of one atom's gathers in pair-term units (cfg1 sweep) */
 #endif
 constexpr float kSplitR = VD_SPLIT_R;
 #ifndef VD_ROLE_NI8
@@ -935,9 +935,11 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
     if (SPLIT && !EXACT && TPP >= 4 && NI < TPP && T.resident) {
         /* balance the two roles with the measured cost ratio of one atom's gathers to one
            pair (kSplitR): the pair subs also take the last xa atoms, or the gather subs the
-           last px share of the pairs.  cfg1 (40 atoms, 608 pairs): xa = 6; swept 0/2/4/6/8/10/12
-           atoms: 1.597/1.577/1.560/1.545/1.550/1.558/1.567 ms; giving the gather subs 10% of
-           the pairs instead: 1.675 ms. */
+           last px share of the pairs.  cfg1 (40 atoms, 608 pairs), before the in-box-only
+           gathers and the packed pose: xa = 6 best of 0/2/4/6/8/10/12 atoms (1.597/1.577/1.560/
+           1.545/1.550/1.558/1.567 ms; 10% of the pairs to the gather subs instead: 1.675 ms);
+           after them, R = 14/16/18.5/21.7/26/30/36/45 gave 1.553/1.501/1.458/1.435/1.419/
+           1.442/1.462/1.484 ms, so R = 26 (xa = 8). */
         const int n = L.n_atoms, np = L.n_pairs;
         const float ex = (float)n - (float)np * (1.0f / kSplitR);
         const int xa = ex > 0.f ? min(n, (int)(0.5f * ex + 0.5f)) : 0;
