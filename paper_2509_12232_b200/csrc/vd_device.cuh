@@ -649,6 +649,9 @@ __device__ __forceinline__ float pair_exact(float dx, float dy, float dz, bool h
     return __fadd_rn(__fadd_rn(well, elec), des);
 }
 
+#ifndef VD_SHARED_RCP
+#define VD_SHARED_RCP 0
+#endif
 #ifndef VD_DESOLV_POLY
 #define VD_DESOLV_POLY 0
 #endif
@@ -691,7 +694,15 @@ __device__ __forceinline__ float2 pair_fast2(float2 dx, float2 dy, float2 dz, fl
     const float2 e = f2(mufu_ex2(earg.x), mufu_ex2(earg.y));
     const float2 den = fma2(f2((float)kDielK), e, f2(1.0f));
     const float2 dd = fmul2(r, fma2(f2((float)kDielA), den, f2((float)kDielB)));
+#if VD_SHARED_RCP
+    /* one MUFU.RCP for both poses: 1/d0 = d1 / (d0 d1), 1/d1 = d0 / (d0 d1).  d = r (A den + B)
+       lies in ~[1.2, 2.4e3], so the product cannot overflow; ~3 ulp instead of 1 (the pair
+       loop is MUFU-bound: 8 -> 7 MUFU per pose pair) */
+    const float qd = mufu_rcp(__fmul_rn(dd.x, dd.y));
+    const float2 rc = fmul2(f2(dd.y, dd.x), f2(qd));
+#else
     const float2 rc = f2(mufu_rcp(dd.x), mufu_rcp(dd.y));
+#endif
     const float2 elec = fmul2(fmul2(f2(cf.z), den), rc);
     const float2 darg = fmul2(r2, f2((float)(-1.4426950408889634 / kDesolvDenom)));
 #if VD_DESOLV_POLY
