@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -151,6 +152,20 @@ static const float4 *ed_for(const vd_grid *gc, int e, int d)
     }
     g->d_ed[{e, d}] = p;
     return p;
+}
+
+cudaError_t raise_smem_limit(const void *kernel, unsigned bytes)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, unsigned> limits;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    unsigned &cur = limits[{dev, kernel}];
+    if (bytes <= cur) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)

@@ -281,7 +281,7 @@ static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const 
 {
     auto k = ga_kernel<EXACT, NPP, TPP>;
     const unsigned bytes = lay.base.bytes;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cudaError_t e = vdi::raise_smem_limit((const void *)k, bytes);
     if (e != cudaSuccess) return e;
     int per_sm = 0, dev = 0, sms = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NPP * TPP, bytes);
@@ -320,7 +320,7 @@ template <bool EXACT, int NPP, int TPP>
 static int occ_t(unsigned bytes)
 {
     auto k = ga_kernel<EXACT, NPP, TPP>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) {
+    if (vdi::raise_smem_limit((const void *)k, bytes) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }

@@ -49,6 +49,10 @@ bool check(cudaError_t e, const char *what);
 bool is_device_ptr(const void *p);
 extern thread_local int64_t g_launches;
 vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map);
+/* Raise a kernel's dynamic shared-memory limit to at least `bytes` on the current device.
+ * The attribute is process-wide, so it only ever grows: a thread launching a smaller ligand
+ * must not lower the limit another thread's launch of the same kernel relies on. */
+cudaError_t raise_smem_limit(const void *kernel, unsigned bytes);
 bool make_packed(vd_grid *g);
 
 }  // namespace vdi

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 #include "vd_internal.h"
@@ -154,16 +155,16 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     /* (the function attributes are per kernel: the dynamic shared-memory limit only ever
        grows, and the carveout is re-applied when another shape changed it) */
     struct Setup { int dev; unsigned bytes; int pct; };
-    static thread_local std::vector<Setup> done_setups;
-    static thread_local std::vector<std::pair<int, unsigned>> max_bytes;  /* (dev, limit set) */
-    static thread_local std::vector<std::pair<int, int>> last_pct;        /* (dev, carveout) */
+    /* process-wide (the attributes are): threads scoring different ligands concurrently must
+       never lower the limit another thread's launch relies on */
+    static std::mutex mu;
+    static std::vector<Setup> done_setups;
+    static std::vector<std::pair<int, int>> last_pct;        /* (dev, carveout) */
+    std::lock_guard<std::mutex> lk(mu);
     int cur_dev = 0;
     cudaGetDevice(&cur_dev);
-    unsigned *limit = nullptr;
     int *carve = nullptr;
-    for (auto &m : max_bytes) if (m.first == cur_dev) limit = &m.second;
     for (auto &c : last_pct) if (c.first == cur_dev) carve = &c.second;
-    if (!limit) { max_bytes.push_back({cur_dev, 0u}); limit = &max_bytes.back().second; }
     if (!carve) { last_pct.push_back({cur_dev, -1}); carve = &last_pct.back().second; }
     const char *l1_env = getenv("VD_L1_KB"), *cv_env = getenv("VD_CARVEOUT");
     for (const Setup &x : done_setups)
@@ -179,12 +180,8 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
             ++vdi::g_launches;
             return cudaGetLastError();
         }
-    cudaError_t e = cudaSuccess;
-    if (lay.bytes > *limit) {
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.bytes);
-        if (e != cudaSuccess) return e;
-        *limit = lay.bytes;
-    }
+    cudaError_t e = vdi::raise_smem_limit((const void *)k, lay.bytes);
+    if (e != cudaSuccess) return e;
     /* Shared-memory carveout: as many CTAs per SM as fit while >= 32 KB of the 256 KB
        L1/shared array stays L1 for the grid gathers (an atom's corners share lines with
        its bonded neighbours').  cfg1 A/B, NPP 32: 1.77 ms at 3 CTAs (63 KB L1) vs 2.00 ms
@@ -252,7 +249,7 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
     cudaError_t e;
 #define VD_P(N)                                                                                   \
     if (npp == N) {                                                                               \
-        e = cudaFuncSetAttribute(pose_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        e = vdi::raise_smem_limit((const void *)pose_kernel<N>, (unsigned)smem);                    \
         if (e == cudaSuccess) pose_kernel<N><<<(unsigned)blocks, N, smem, st>>>(L, genes, P, ngenes, lay, 1.0f /* run-time: see xadd2 */, out); \
     }
     VD_P(64) else VD_P(32) else VD_P(16) else return cudaErrorInvalidConfiguration;

@@ -313,3 +313,22 @@ def test_alternating_ligand_sizes_reuse_launch_setup(cuda, mode):
     again = cuda[mode].score_population_arrays(big["genes"], big["ctx"])
     for x, y in zip(first, again):
         assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_concurrent_threads_different_ligands(cuda):
+    """The reference's screen_batch drives one backend from several Python threads
+    (vd/screening.py:116-161): concurrent calls on ligands of different sizes must neither
+    fail (kernel attributes are process-wide) nor change any result."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cases = [fx.pop_case(n) for n in ("cfg1", "cfg0", "big", "refgen")]
+    want = [cuda["fast"].score_population_arrays(c["genes"], c["ctx"]) for c in cases]
+
+    def work(k):
+        c = cases[k % len(cases)]
+        return k % len(cases), cuda["fast"].score_population_arrays(c["genes"], c["ctx"])
+
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        for k, got in ex.map(work, range(24)):
+            for x, y in zip(got, want[k]):
+                assert np.array_equal(np.asarray(x), np.asarray(y))
