@@ -138,6 +138,10 @@ __device__ __forceinline__ float2 sub2(float2 a, float2 b)
 }
 /* Exact packed ops (VD_POSE_PACKED): FMUL2 rounds each product; sums are written as
  * fma(a, one, b) / fma(b, -one, a) with a run-time one, which ptxas cannot contract. */
+#ifndef VD_FRAG_UNROLL
+#define VD_FRAG_UNROLL 2   /* fragment loop: 2 vs 4 vs 8: 1.411 / 1.419 / 1.418 ms (cfg1) */
+#endif
+constexpr int kFragUnroll = VD_FRAG_UNROLL;
 #ifndef VD_POSE_PACKED
 #define VD_POSE_PACKED 1   /* pose stage alone 0.441 -> 0.404 ms per 1M cfg1 poses; whole
                               kernel 1.557 -> 1.543 ms; cfg2 screen +1.4% */
@@ -301,7 +305,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
         }
         const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
         const float2 OMC = sub2(f2(1.0f), C);
-#pragma unroll 4
+#pragma unroll kFragUnroll
         for (int f = tr.z + sub; f < tr.w; f += TPP) {
             const int i = L.frag[f];
 #if VD_POSE_PACKED
