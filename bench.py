@@ -42,7 +42,7 @@ WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
 # dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
 # committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
-TRAFFIC_BYTES = 166.08e6 + 21.77e6
+TRAFFIC_BYTES = 166.09e6 + 22.35e6
 TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,64,4>)"
 
 
