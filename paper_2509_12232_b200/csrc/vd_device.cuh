@@ -348,14 +348,40 @@ __device__ __forceinline__ float lerp_(float a, float b, float t)
     return __fadd_rn(__fmul_rn(a, __fsub_rn(1.0f, t)), __fmul_rn(b, t));
 }
 
-template <bool EXACT>
+#ifndef VD_PLAIN_ZPAIR
+#define VD_PLAIN_ZPAIR 1
+#endif
+/* (v[z], v[z+1]) of the plain layout: one LDG.64 when the pair is 8-B aligned, else two
+ * LDG.32 (predicated per lane) -- 1.5 requests per corner pair instead of 2 */
+template <bool ZP>
+__device__ __forceinline__ float2 ld_zpair(const float *p)
+{
+    float2 v;
+#if VD_PLAIN_ZPAIR
+    if (ZP) {
+    asm("{\n\t.reg .pred q;\n\t"
+        "setp.eq.b32 q, %3, 0;\n\t"
+        "@q ld.global.nc.v2.f32 {%0,%1}, [%2];\n\t"
+        "@!q ld.global.nc.f32 %0, [%2];\n\t"
+        "@!q ld.global.nc.f32 %1, [%2+4];\n\t}"
+        : "=f"(v.x), "=f"(v.y)
+        : "l"(p), "r"((int)(reinterpret_cast<uintptr_t>(p) & 7u)));
+    return v;
+    }
+#endif
+    v.x = __ldg(p);
+    v.y = __ldg(p + 1);
+    return v;
+}
+
+template <bool EXACT, bool ZP = false>
 __device__ __forceinline__ float trilerp(const float *__restrict__ m, int idx, int nz, int nyz,
                                          float fx, float fy, float fz)
 {
-    const float v000 = __ldg(m + idx), v001 = __ldg(m + idx + 1);
-    const float v010 = __ldg(m + idx + nz), v011 = __ldg(m + idx + nz + 1);
-    const float v100 = __ldg(m + idx + nyz), v101 = __ldg(m + idx + nyz + 1);
-    const float v110 = __ldg(m + idx + nyz + nz), v111 = __ldg(m + idx + nyz + nz + 1);
+    const float2 a = ld_zpair<ZP>(m + idx), b = ld_zpair<ZP>(m + idx + nz);
+    const float2 c = ld_zpair<ZP>(m + idx + nyz), d = ld_zpair<ZP>(m + idx + nyz + nz);
+    const float v000 = a.x, v001 = a.y, v010 = b.x, v011 = b.y;
+    const float v100 = c.x, v101 = c.y, v110 = d.x, v111 = d.y;
     const float c00 = lerp_<EXACT>(v000, v100, fx), c10 = lerp_<EXACT>(v010, v110, fx);
     const float c01 = lerp_<EXACT>(v001, v101, fx), c11 = lerp_<EXACT>(v011, v111, fx);
     const float c0 = lerp_<EXACT>(c00, c10, fy), c1 = lerp_<EXACT>(c01, c11, fy);
@@ -548,7 +574,7 @@ __device__ __forceinline__ float finish_packed(const Gather &g, float q, float d
 }
 
 /* One atom of one pose against the plain (n_maps, nx, ny, nz) layout. */
-template <bool EXACT>
+template <bool EXACT, bool ZP = false>
 __device__ __forceinline__ float atom_term(const GridView &G, const float *__restrict__ tmap,
                                            const float *__restrict__ emap,
                                            const float *__restrict__ dmap, float q, float dsf,
@@ -559,9 +585,9 @@ __device__ __forceinline__ float atom_term(const GridView &G, const float *__res
     cell_of(G, x, y, z, pen, g, idx, zy);
     if (EXACT && !g.inb) return g.pterm;
     const int nyz = G.ny * G.nz;
-    const float vt = trilerp<true>(tmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
-    const float ve = trilerp<true>(emap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
-    const float vd = trilerp<true>(dmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
+    const float vt = trilerp<true, ZP>(tmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
+    const float ve = trilerp<true, ZP>(emap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
+    const float vd = trilerp<true, ZP>(dmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
     const float gterm = __fadd_rn(__fadd_rn(vt, __fmul_rn(q, ve)), __fmul_rn(dsf, vd));
     return g.inb ? gterm : g.pterm;
 }
@@ -627,8 +653,10 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
         const float2 a2 = L.atom2[i];
         const float *tmap = G.maps + G.mstride * __float_as_int(a2.y);
         const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
-        const float t0 = atom_term<EXACT>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.x, y.x, z.x);
-        const float t1 = atom_term<EXACT>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.y, y.y, z.y);
+        /* z-pair loads (1.5 requests per corner pair) in the unpipelined score kernel: cfg4
+           scoring 46.1 -> 48.8 M poses/s; the GA path keeps scalar loads (-16% with them) */
+        const float t0 = atom_term<EXACT, !PIPE>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.x, y.x, z.x);
+        const float t1 = atom_term<EXACT, !PIPE>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.y, y.y, z.y);
         e0 = __dadd_rn(e0, (double)t0);
         e1 = __dadd_rn(e1, (double)t1);
     }
