@@ -583,7 +583,7 @@ __device__ __forceinline__ float atom_term(const GridView &G, const float *__res
     Gather g;
     int idx, zy;
     cell_of(G, x, y, z, pen, g, idx, zy);
-    if (EXACT && !g.inb) return g.pterm;
+    if ((EXACT || ZP) && !g.inb) return g.pterm;  /* ZP (score kernel): out-of-box lanes skip the gathers */
     const int nyz = G.ny * G.nz;
     const float vt = trilerp<true, ZP>(tmap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
     const float ve = trilerp<true, ZP>(emap, idx, G.nz, nyz, g.fx, g.fy, g.fz);
