@@ -351,6 +351,10 @@ __device__ __forceinline__ float lerp_(float a, float b, float t)
 #ifndef VD_PLAIN_ZPAIR
 #define VD_PLAIN_ZPAIR 1
 #endif
+#ifndef VD_PLAIN_UNROLL
+#define VD_PLAIN_UNROLL 1
+#endif
+constexpr int kPlainUnroll = VD_PLAIN_UNROLL;
 /* (v[z], v[z+1]) of the plain layout: one LDG.64 when the pair is 8-B aligned, else two
  * LDG.32 (predicated per lane) -- 1.5 requests per corner pair instead of 2 */
 template <bool ZP>
@@ -600,11 +604,15 @@ __device__ __forceinline__ float atom_term(const GridView &G, const float *__res
  * atom i is interpolated.  That doubles the live gather state (152 vs 94 registers in
  * score_kernel); the score kernel runs unpipelined and covers the latency with its 12
  * resident warps, the GA kernel (register-bound by its other stages anyway) pipelines. */
-template <bool EXACT, int NPP, int TPP, bool PIPE>
+/* LAY: 0 = both gather paths (run-time choice), 1 = packed grid only, 2 = plain grid only.
+ * The kernels are instantiated per layout so that neither path's registers weigh on the
+ * other (with both compiled in, the plain path's z-pair gathers took the score kernel from
+ * 121 to 168 registers, 1 CTA/SM). */
+template <bool EXACT, int NPP, int TPP, bool PIPE, int LAY = 0>
 __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, const float2 *S,
                                        int sub, int ia, int ib, double &e0, double &e1)
 {
-    if (G.yz != nullptr && !EXACT) {
+    if (LAY != 2 && G.yz != nullptr && !EXACT) {
         const int n = ib;
         int i = ia + sub;
         if (i >= n) return;
@@ -645,18 +653,20 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
         }
         return;
     }
+    if constexpr (LAY == 1 && !EXACT) return;
     const float *emap = G.maps + G.mstride * L.elec_map;
     const float *dmap = G.maps + G.mstride * L.desolv_map;
-#pragma unroll 2
+    /* z-pair loads and the out-of-box early return, atom loop not unrolled: unrolled x2 the
+       z-pair gathers raised the score kernel to 168 registers (1 CTA/SM: cfg1 1.41 -> 2.09 ms)
+       and cost the GA 7-16%; not unrolled, cfg4 GA 1,297 -> 1,600 ligands/s */
+#pragma unroll kPlainUnroll
     for (int i = ia + sub; i < ib; i += TPP) {
         const float4 a = L.atom[i];
         const float2 a2 = L.atom2[i];
         const float *tmap = G.maps + G.mstride * __float_as_int(a2.y);
         const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
-        /* z-pair loads (1.5 requests per corner pair) in the unpipelined score kernel: cfg4
-           scoring 46.1 -> 48.8 M poses/s; the GA path keeps scalar loads (-16% with them) */
-        const float t0 = atom_term<EXACT, !PIPE>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.x, y.x, z.x);
-        const float t1 = atom_term<EXACT, !PIPE>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.y, y.y, z.y);
+        const float t0 = atom_term<EXACT, true>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.x, y.x, z.x);
+        const float t1 = atom_term<EXACT, true>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.y, y.y, z.y);
         e0 = __dadd_rn(e0, (double)t0);
         e1 = __dadd_rn(e1, (double)t1);
     }
@@ -963,7 +973,7 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
 }
 
 /* inter + intra of both poses (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT>
+template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
                                         double &a0, double &a1)
@@ -989,18 +999,18 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
         const unsigned px = ex < 0.f ? (unsigned)(-ex * kSplitR / (2.0f * (float)np) * 65536.0f) : 0u;
         const int acut = n - xa;
         if (sub < NI) {
-            inter2<EXACT, NPP, NI, PIPE>(L, G, S, sub, 0, acut, e0, e1);
+            inter2<EXACT, NPP, NI, PIPE, LAY>(L, G, S, sub, 0, acut, e0, e1);
             if (px) intra2<EXACT, NPP, NA>(L, S, T, sub, a0, a1, 65536u - px + sub * px / NI,
                                            65536u - px + (sub + 1) * px / NI);
         } else {
             const int s = sub - NI;
             intra2<EXACT, NPP, NA>(L, S, T, s, a0, a1, s * (65536u - px) / NA,
                                    (s + 1) * (65536u - px) / NA);
-            if (acut < n) inter2<EXACT, NPP, NA, PIPE>(L, G, S, s, acut, n, e0, e1);
+            if (acut < n) inter2<EXACT, NPP, NA, PIPE, LAY>(L, G, S, s, acut, n, e0, e1);
         }
         return;
     }
-    inter2<EXACT, NPP, TPP, PIPE>(L, G, S, sub, 0, L.n_atoms, e0, e1);
+    inter2<EXACT, NPP, TPP, PIPE, LAY>(L, G, S, sub, 0, L.n_atoms, e0, e1);
     intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }
 

@@ -178,7 +178,7 @@ constexpr int ga_minb(int threads)
     return VD_GA_REGS > 0 ? (65536 / (threads * VD_GA_REGS) > 0 ? 65536 / (threads * VD_GA_REGS) : 1)
                           : VD_GA_MINB;
 }
-template <bool EXACT, int NPP, int TPP>
+template <bool EXACT, int NPP, int TPP, int LAY>
 __global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, int count,
                                                       GaDev P, uint64_t seed, int64_t base,
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridVie
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, LAY>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
@@ -279,7 +279,9 @@ static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const 
                                const GaLayout &lay, const GaOut &out, cudaStream_t st,
                                int *d_work, double **gene_buf, int *n_ctas)
 {
-    auto k = ga_kernel<EXACT, NPP, TPP>;
+    auto k = ga_kernel<EXACT, NPP, TPP, 2>;  /* plain grid (and every exact launch) */
+    if constexpr (!EXACT)
+        if (Gv.yz != nullptr) k = ga_kernel<EXACT, NPP, TPP, 1>;  /* packed grid */
     const unsigned bytes = lay.base.bytes;
     cudaError_t e = vdi::raise_smem_limit((const void *)k, bytes);
     if (e != cudaSuccess) return e;
@@ -317,9 +319,11 @@ cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const Li
 }
 
 template <bool EXACT, int NPP, int TPP>
-static int occ_t(unsigned bytes)
+static int occ_t(unsigned bytes, bool packed)
 {
-    auto k = ga_kernel<EXACT, NPP, TPP>;
+    auto k = ga_kernel<EXACT, NPP, TPP, 2>;
+    if constexpr (!EXACT)
+        if (packed) k = ga_kernel<EXACT, NPP, TPP, 1>;
     if (vdi::raise_smem_limit((const void *)k, bytes) != cudaSuccess) {
         cudaGetLastError();
         return 0;
@@ -333,10 +337,10 @@ static int occ_t(unsigned bytes)
 }
 
 /* resident CTAs per SM for a GA shape (registers and shared memory both count) */
-int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes)
+int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes, bool packed)
 {
 #define VD_O(EX, N, T) \
-    if (exact == EX && npp == N && tpp == T) return occ_t<EX, N, T>(bytes)
+    if (exact == EX && npp == N && tpp == T) return occ_t<EX, N, T>(bytes, packed)
     VD_O(true, 64, 1); VD_O(true, 32, 1); VD_O(true, 16, 1);
     VD_O(false, 64, 1); VD_O(false, 32, 1); VD_O(false, 16, 1);
     VD_O(false, 64, 2); VD_O(false, 32, 2); VD_O(false, 16, 2);
@@ -387,6 +391,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         set_error("vd_dock_batch: gstride smaller than 7 + max torsions");
         return -1;
     }
+    const vd::GridView gv = vdi::grid_view(g, s->elec_map, s->desolv_map);
     std::vector<int> order;
     struct Launch {
         int off, cnt, npp, tpp;
@@ -426,7 +431,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra, pmax);
             if (lay.base.bytes > 227u * 1024u) continue;
             if (npp * L.tpp < 32) continue;  /* block_argmin's shuffles need whole warps */
-            int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes) * npp * L.tpp / 32;
+            int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes, gv.yz != nullptr) * npp * L.tpp / 32;
             if (npp == 64) warps -= 4;  /* measured: 64 needs clearly more warps to win */
             /* (unlike the score kernel, the GA prefers one 32 x 8 CTA to two 16 x 8 ones at
                the same warps for cfg4: 1239 vs 880 ligands/s -- its per-tile barriers and
@@ -490,7 +495,6 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     vd::GaOut o;
     o.best_total = d_bt; o.best_inter = d_be; o.best_intra = d_ba; o.best_genes = d_bg;
     o.gstride = gstride; o.trace = d_tr; o.n_evals = d_ne;
-    const vd::GridView gv = vdi::grid_view(g, s->elec_map, s->desolv_map);
     /* Buckets run concurrently, largest atoms first, each on its own stream forked from st:
        a persistent launch ends with a tail of SMs whose CTAs found the work counter empty,
        and the next bucket's CTAs fill them instead of waiting for the whole launch to drain.

@@ -26,7 +26,7 @@
 
 namespace vd {
 
-template <bool EXACT, int NPP, int TPP>
+template <bool EXACT, int NPP, int TPP, int LAY>
 __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
                                                          const double *__restrict__ genes,
                                                          const float *__restrict__ poses,
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
 #ifndef VD_TEST_STAGE
-    energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0>(L, G, S, T, sub, e0, e1, a0, a1);
+    energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0, LAY>(L, G, S, T, sub, e0, e1, a0, a1);
 #else  /* (timing only) the pose stage alone */
     e0 = S[0].x; e1 = S[NPP].y;
 #endif
@@ -149,26 +149,29 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
                             double *intra, float *total, cudaStream_t st)
 {
     const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, NPP, TPP, 0, L.n_pairs);
-    auto k = score_kernel<EXACT, NPP, TPP>;
+    auto k = score_kernel<EXACT, NPP, TPP, 2>;  /* plain grid (and every exact launch) */
+    if constexpr (!EXACT)
+        if (G.yz != nullptr) k = score_kernel<EXACT, NPP, TPP, 1>;  /* packed grid */
     /* the attribute / occupancy set-up below costs ~10 driver calls; a host-buffer batch
        launches once per pipeline chunk, so it is done once per (device, shared-memory size) */
     /* (the function attributes are per kernel: the dynamic shared-memory limit only ever
        grows, and the carveout is re-applied when another shape changed it) */
-    struct Setup { int dev; unsigned bytes; int pct; };
+    struct Setup { int dev; const void *fn; unsigned bytes; int pct; };
     /* process-wide (the attributes are): threads scoring different ligands concurrently must
        never lower the limit another thread's launch relies on */
     static std::mutex mu;
     static std::vector<Setup> done_setups;
-    static std::vector<std::pair<int, int>> last_pct;        /* (dev, carveout) */
+    struct Carve { int dev; const void *fn; int pct; };
+    static std::vector<Carve> last_pct;
     std::lock_guard<std::mutex> lk(mu);
     int cur_dev = 0;
     cudaGetDevice(&cur_dev);
     int *carve = nullptr;
-    for (auto &c : last_pct) if (c.first == cur_dev) carve = &c.second;
-    if (!carve) { last_pct.push_back({cur_dev, -1}); carve = &last_pct.back().second; }
+    for (auto &c : last_pct) if (c.dev == cur_dev && c.fn == (const void *)k) carve = &c.pct;
+    if (!carve) { last_pct.push_back({cur_dev, (const void *)k, -1}); carve = &last_pct.back().pct; }
     const char *l1_env = getenv("VD_L1_KB"), *cv_env = getenv("VD_CARVEOUT");
     for (const Setup &x : done_setups)
-        if (x.dev == cur_dev && x.bytes == lay.bytes && !l1_env && !cv_env) {
+        if (x.dev == cur_dev && x.fn == (const void *)k && x.bytes == lay.bytes && !l1_env && !cv_env) {
             if (*carve != x.pct) {
                 cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, x.pct);
                 if (e != cudaSuccess) return e;
@@ -202,7 +205,7 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     if (e != cudaSuccess) return e;
     *carve = pct;
-    if (done_setups.size() < 64) done_setups.push_back({cur_dev, lay.bytes, pct});
+    if (done_setups.size() < 64) done_setups.push_back({cur_dev, (const void *)k, lay.bytes, pct});
     const int64_t per_cta = 2 * NPP;
     const int64_t blocks = (P + per_cta - 1) / per_cta;
     if (getenv("VD_VERBOSE"))
