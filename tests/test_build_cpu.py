@@ -1,0 +1,46 @@
+"""Build-time guards on the hot kernels' resources (parsed from the ptxas -v log of the last
+build, paper_2509_12232_b200/csrc/build.log).  The score kernel's occupancy is 2 CTAs x 256
+threads per SM, which needs <= 128 registers: a change that pushed it to 168 registers once
+halved the resident CTAs and cost cfg1 48% without failing any numerical test."""
+
+from __future__ import annotations
+
+import re
+from pathlib import Path
+
+import pytest
+
+LOG = Path(__file__).resolve().parents[1] / "paper_2509_12232_b200" / "csrc" / "build.log"
+
+
+def _resources(mangled_prefix: str):
+    if not LOG.exists():
+        pytest.skip("no build log (run __graft_entry__.build() first)")
+    text = LOG.read_text()
+    i = text.find(f"Compiling entry function '{mangled_prefix}")
+    if i < 0:
+        pytest.skip(f"{mangled_prefix} not in the build log")
+    block = text[i:i + 800]
+    regs = int(re.search(r"Used (\d+) registers", block).group(1))
+    spill = int(re.search(r"(\d+) bytes spill stores", block).group(1))
+    return regs, spill
+
+
+@pytest.mark.parametrize("kernel", [
+    "_ZN2vd12score_kernelILb0ELi64ELi4ELi1E",   # cfg1 bench shape, packed grid
+    "_ZN2vd12score_kernelILb0ELi32ELi4ELi1E",
+    "_ZN2vd12score_kernelILb0ELi16ELi8ELi2E",   # cfg4 shape, plain grid
+])
+def test_score_kernel_fits_two_ctas_without_spills(kernel):
+    regs, spill = _resources(kernel)
+    assert regs <= 128, f"{kernel}: {regs} registers (2 CTAs x 256 threads need <= 128)"
+    assert spill == 0, f"{kernel}: {spill} bytes of spills"
+
+
+@pytest.mark.parametrize("kernel", [
+    "_ZN2vd9ga_kernelILb0ELi32ELi4ELi1E",   # cfg2 buckets, packed grid
+    "_ZN2vd9ga_kernelILb0ELi32ELi8ELi2E",   # cfg4, plain grid
+])
+def test_ga_kernel_has_no_spills(kernel):
+    regs, spill = _resources(kernel)
+    assert spill == 0, f"{kernel}: {spill} bytes of spills at {regs} registers"
