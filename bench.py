@@ -42,8 +42,8 @@ WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
 # dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
 # committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
-TRAFFIC_BYTES = 166.09e6 + 22.35e6
-TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,64,4>)"
+TRAFFIC_BYTES = 166.96e6 + 20.75e6
+TRAFFIC_SRC = "profiles/r1_score_kernel.md (ncu --set full, one launch of score_kernel<0,64,4,1>)"
 
 
 def env_int(k, d):
@@ -116,7 +116,7 @@ def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx
             "ceiling_poses_per_s": fp32_peak * 1e12 / fpp}
     out = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
            "frac": achieved_tf / fp32_peak, "traffic": TRAFFIC_BYTES,
-           "traffic_source": TRAFFIC_SRC, "kernel": "vd::score_kernel<false,64,4>",
+           "traffic_source": TRAFFIC_SRC, "kernel": "vd::score_kernel<false,64,4,1> (packed-grid instantiation)",
            "fp32": fp32, "arithmetic_intensity_flop_per_byte": fpp / bpp}
     if peaks:
         l2 = peaks["l2_gather_gbs"]
