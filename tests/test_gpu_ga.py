@@ -230,3 +230,32 @@ def test_exact_ga_operator_variants_match_oracle(cuda, kw):
     assert np.array_equal(res.trace.view(np.uint32), trace.view(np.uint32))
     assert np.array_equal(res.best_genotype, g)
     assert res.n_evaluations == ne
+
+
+@pytest.mark.parametrize("layout", ["plain", "zpair", "brick"])
+def test_fast_mode_ga_identical_on_every_grid_layout(cuda, layout, monkeypatch):
+    """The GA kernel is instantiated per grid layout (packed: pipelined brick / z-pair
+    gathers; plain: z-pair loads with the out-of-box early return, e.g. cfg4's 126^3 grid).
+    Corner values, lerps and the atom summation order are the same, so a fast-mode GA run
+    is bit-identical on every layout."""
+    from paper_2509_12232_b200 import gridmaps
+    from paper_2509_12232_b200.backend import CudaBackend
+    from paper_2509_12232_b200.context import prepare_context
+    from paper_2509_12232_b200.ga import GaConfig, dock
+
+    env = {"plain": ("VD_NO_PACK", "1"), "zpair": ("VD_BRICK_BUDGET_MB", "0"),
+           "brick": ("VD_BRICK_BUDGET_MB", "100000")}
+    c = fx.pop_case("cfg1")
+    cfg = GaConfig(population_size=64, generations=8, seed=21)
+
+    def run(lay):
+        monkeypatch.setenv(*env[lay])
+        g2 = gridmaps.GridMapSet(c["grid"].spec, dict(c["grid"].maps))  # fresh device grid
+        ctx = prepare_context(c["topo"], g2)
+        r = dock(c["topo"], g2, cfg, backend=CudaBackend(mode="fast", device=0), context=ctx)
+        monkeypatch.undo()
+        return r
+
+    got, ref = run(layout), run("plain" if layout != "plain" else "brick")
+    assert np.array_equal(got.trace.view(np.uint32), ref.trace.view(np.uint32))
+    assert np.array_equal(got.best_genotype, ref.best_genotype)
