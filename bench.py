@@ -423,7 +423,8 @@ def screening_leg(args, rank, world, dist, dev):
     return {"metric": "ligands docked/sec", "value": n / t_max, "unit": "ligands/s",
             "pose_evals_per_s": evals / t_max, "ligands": n, "ms": 1e3 * t_max,
             "ga": "pop 256 x 200 generations (cfg2 distribution, 64^3 grid, 3000-atom receptor)",
-            "workload": "cfg2-screen-10k" if n == 10000 else f"cfg2-distribution x{n}",
+            "workload": ("cfg2-screen-10k" if n == 10000 else "cfg3-screen-100k" if n == 100000
+                         else f"cfg2-distribution x{n}"),
             "gathered_records": int(rec.shape[0]), "gather_ms": round(1e3 * t_gather, 3),
             "host_prep_s_per_rank": round(prep_s, 3),
             "timing": "CUDA events around vd_dock_batch (one persistent GA launch per atom-count bucket, buckets concurrent), max over ranks",
