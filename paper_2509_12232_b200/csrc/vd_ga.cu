@@ -159,6 +159,7 @@ __device__ void breed_child(const GaDev &P, int G, const double *cur, const floa
 struct GaLayout {
     SmemLayout base;          /* pose tile + pair tiles (+ reduction) for the largest ligand */
     unsigned off_fit, off_e, off_a, off_taken;
+    int r3 = 0;               /* host: launch the 3-CTA register-budget variant (LAY 3) */
 };
 
 #ifndef VD_GA_MINB
@@ -178,8 +179,11 @@ constexpr int ga_minb(int threads)
     return VD_GA_REGS > 0 ? (65536 / (threads * VD_GA_REGS) > 0 ? 65536 / (threads * VD_GA_REGS) : 1)
                           : VD_GA_MINB;
 }
+/* LAY: 1 packed grid, 2 plain grid, 3 packed grid with a 3-CTA register budget (168
+ * registers instead of 245: for 32 x 4 tiles of small ligands, whose shared memory leaves
+ * room for a third CTA that the full register budget does not) */
 template <bool EXACT, int NPP, int TPP, int LAY>
-__global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+__global__ void __launch_bounds__(NPP *TPP, LAY == 3 ? 3 : ga_minb(NPP *TPP)) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, int count,
                                                       GaDev P, uint64_t seed, int64_t base,
                                                       int *work, double *gene_buf, int gmax,
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(NPP *TPP, ga_minb(NPP *TPP)) ga_kernel(GridVie
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, LAY>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, (LAY == 3 ? 1 : LAY)>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
                 reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
@@ -282,6 +286,8 @@ static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const 
     auto k = ga_kernel<EXACT, NPP, TPP, 2>;  /* plain grid (and every exact launch) */
     if constexpr (!EXACT)
         if (Gv.yz != nullptr) k = ga_kernel<EXACT, NPP, TPP, 1>;  /* packed grid */
+    if constexpr (!EXACT && NPP == 32 && TPP == 4)
+        if (Gv.yz != nullptr && lay.r3) k = ga_kernel<EXACT, NPP, TPP, 3>;
     const unsigned bytes = lay.base.bytes;
     cudaError_t e = vdi::raise_smem_limit((const void *)k, bytes);
     if (e != cudaSuccess) return e;
@@ -337,6 +343,21 @@ static int occ_t(unsigned bytes, bool packed)
 }
 
 /* resident CTAs per SM for a GA shape (registers and shared memory both count) */
+static int ga_occupancy_r3(unsigned bytes)
+{
+    auto k = ga_kernel<false, 32, 4, 3>;
+    if (vdi::raise_smem_limit((const void *)k, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per_sm;
+}
+
 int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes, bool packed)
 {
 #define VD_O(EX, N, T) \
@@ -432,6 +453,16 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             if (lay.base.bytes > 227u * 1024u) continue;
             if (npp * L.tpp < 32) continue;  /* block_argmin's shuffles need whole warps */
             int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes, gv.yz != nullptr) * npp * L.tpp / 32;
+            lay.r3 = 0;
+            if (!exact && npp == 32 && L.tpp == 4 && gv.yz != nullptr && !getenv("VD_GA_NO_R3")) {
+                /* small ligands: a third CTA fits in shared memory but not in 245 registers
+                   (<= 32 atoms: +5-6% ligands/s measured with the 168-register budget) */
+                const int w3 = vd::ga_occupancy_r3(lay.base.bytes) * 4;
+                if (w3 > warps) {
+                    warps = w3;
+                    lay.r3 = 1;
+                }
+            }
             if (npp == 64) warps -= 4;  /* measured: 64 needs clearly more warps to win */
             /* (unlike the score kernel, the GA prefers one 32 x 8 CTA to two 16 x 8 ones at
                the same warps for cfg4: 1239 vs 880 ligands/s -- its per-tile barriers and
