@@ -73,6 +73,10 @@ int vd_grid_build(const float *rec_xyz /* (3, n_rec) */, const int32_t *rec_type
                   const int32_t *probe, int n_probe, const double origin[3], double spacing,
                   int nx, int ny, int nz, const vd_weights *w, double cutoff, vd_grid **out);
 int vd_grid_n_maps(const vd_grid *g);
+/* gather layout chosen at creation: plain maps only, type maps as
+ * yz-bricks, or as z-pairs (both with elec/desolv bricks); -1 for a NULL handle */
+enum vd_layout { VD_LAYOUT_PLAIN = 0, VD_LAYOUT_BRICK = 1, VD_LAYOUT_ZPAIR = 2 };
+int vd_grid_layout(const vd_grid *g);
 int vd_grid_download(const vd_grid *g, float *out /* (n_maps, nx, ny, nz) host */);
 int vd_grid_destroy(vd_grid *g);
 
@@ -160,6 +164,29 @@ int vd_synth_fill(uint64_t seed, int64_t first, int count, int h_lo, int h_hi, d
 
 /* device-side counters of the last call on this thread (kernel launches) */
 int vd_last_launch_count(int64_t *launches);
+
+/* ---- test probes (parity checks of the GA's device randomness) ------------
+ * They run the GA kernel's own device functions on chosen inputs, so the
+ * oracle (oracle/or_rng.c, oracle/vd_ga_oracle.c) can check them draw for draw.
+ * Counter map: block (slot/4, idx, gen, phase), word slot%4.
+ * (vd_debug_pose_genes, below, does the same for the fast score kernel's pose stage.)
+ *   vd_debug_rng kind 0: uint64 words [n_idx][n_slot] of (phase, gen);
+ *                kind 1: f64 normals [n_idx][n_slot], component = slot
+ *   vd_debug_ga_init:  init_population (vd/ga.py:90-109) -> [pop][7+T]
+ *   vd_debug_ga_breed: the pop - elitism bred children of next_generation
+ *                      (vd/ga.py:139-174) -> [pop - elitism][7+T]
+ * All buffers are host memory; the calls synchronise. */
+int vd_debug_rng(int kind, uint64_t seed, uint64_t lig_index, int phase, int64_t gen,
+                 int64_t n_idx, int n_slot, void *out);
+int vd_debug_ga_init(const vd_ga_params *p, int n_torsions, uint64_t seed, uint64_t lig_index,
+                     double *out);
+int vd_debug_ga_breed(const vd_ga_params *p, int n_torsions, const double *cur,
+                      const float *fitness, int gen, uint64_t seed, uint64_t lig_index,
+                      double *children);
+/* the fast score kernel's pose stage (pose tile of TPP = 4 or 8 sub-threads per pose pair,
+ * shared scratch, barrier-ordered torsion chain) written out as (P, 3, N) f32 poses */
+int vd_debug_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, int tpp,
+                        float *poses);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,8 @@ def lib():
         L.or_cos2pi.restype = C.c_double
         L.or_normal.argtypes = [C.c_uint64] * 6
         L.or_normal.restype = C.c_double
+        L.or_rng_words.argtypes = [C.c_uint64, C.c_uint64, i32, i64, i64, i64, vp]
+        L.or_rng_normals.argtypes = [C.c_uint64, C.c_uint64, i32, i64, i64, i64, vp]
         L.or_init_population.argtypes = [vp, i32, C.c_uint64, C.c_uint64, vp]
         L.or_next_generation.argtypes = [vp, i32, vp, vp, i32, C.c_uint64, C.c_uint64, vp, vp]
         L.or_dock.argtypes = [vp, vp, C.c_uint64, C.c_uint64, f32, vp, vp, vp, vp, vp, vp]
@@ -160,6 +162,50 @@ class Ligand:
         self.torsional32 = np.float32(ctx.torsional32)
 
 
+class _CsrContext:
+    """One ligand of a vd_ligand_arrays CSR set, in the ScoringContext field names."""
+
+    def __init__(self, a: dict, l: int, spec):
+        s0, s1 = int(a["atom_start"][l]), int(a["atom_start"][l + 1])
+        p0, p1 = int(a["pair_start"][l]), int(a["pair_start"][l + 1])
+        t0, t1 = int(a["tors_start"][l]), int(a["tors_start"][l + 1])
+        self.n_atoms = s1 - s0
+        self.charge = a["charge"][s0:s1]
+        self.desolv_factor = a["desolv_factor"][s0:s1]
+        self.pose_centered0 = a["centered0"][3 * s0:3 * s1].reshape(-1, 3).T  # atom-major -> (3, n)
+        self.atom_map = a["atom_map"][s0:s1]
+        for f in ("pair_i", "pair_j", "pair_a", "pair_b", "pair_qq", "pair_desolv", "pair_hb"):
+            setattr(self, f, a[f][p0:p1])
+        self.n_pairs = p1 - p0
+        lo, hi = a["frag_lo"][t0:t1], a["frag_hi"][t0:t1]
+        f0 = int(lo[0]) if t1 > t0 else 0
+        self.frag_start = np.concatenate([[0], np.cumsum(hi - lo)]).astype(np.int32)
+        self.frag_index = np.concatenate([a["frag_index"][x:y] for x, y in zip(lo, hi)]) \
+            if t1 > t0 else np.empty(0, np.int32)
+        assert t1 == t0 or np.array_equal(lo - f0, self.frag_start[:-1])
+        self.frag_axis_a, self.frag_axis_b = a["axis_a"][t0:t1], a["axis_b"][t0:t1]
+        self.dims = tuple(int(d) for d in spec.dims)
+        self.box_lo = np.asarray(spec.origin, np.float32)
+        self.box_hi = np.asarray(spec.upper, np.float32)
+        self.spacing = np.float32(spec.spacing)
+        self.penalty_scale = np.float32(a["penalty_scale"][l])
+        self.intra_cutoff2 = np.float32(a["intra_cutoff2"][l])
+        self.torsional32 = np.float32(a["torsional32"][l])
+
+
+def ligands_from_arrays(arrays: dict, maps: np.ndarray, spec, which=None) -> list:
+    """Oracle ligands over a shared (m, nx, ny, nz) map stack for ligands `which` (default all)
+    of a vd_ligand_arrays CSR set (hostprep.prepare_batch, bit-identical to prepare_context),
+    with the same global map indices the device set uses."""
+    stack = np.ascontiguousarray(maps, dtype=np.float32)
+    n = len(arrays["atom_start"]) - 1
+    out = []
+    for l in (range(n) if which is None else which):
+        c = _CsrContext(arrays, int(l), spec)
+        out.append(Ligand(c, stack, c.atom_map, arrays["_elec"], arrays["_desolv"]))
+    return out
+
+
 def dock_population(lig: Ligand, genes: np.ndarray, n_threads: int = 1):
     """(inter64, intra64, total32) per genotype row -- SimdBackend.dock_population + totals."""
     g = np.ascontiguousarray(genes, dtype=np.float64)
@@ -220,6 +266,23 @@ def build_grid(protein, origin, spacing, dims, probe_types, weights, table, cuto
 def philox_block(counter, key) -> np.ndarray:
     out = np.empty(4, np.uint64)
     lib().or_philox_block(*[int(c) for c in counter], int(key[0]), int(key[1]), out.ctypes.data)
+    return out
+
+
+def rng_words(seed: int, lig_index: int, phase: int, gen: int, n_idx: int,
+              n_slot: int) -> np.ndarray:
+    """Words of the restated GA stream (or_rng.c): [idx][slot] at (phase, gen)."""
+    out = np.empty((n_idx, n_slot), np.uint64)
+    lib().or_rng_words(int(seed), int(lig_index), int(phase), int(gen), int(n_idx), int(n_slot),
+                       out.ctypes.data)
+    return out
+
+
+def rng_normals(seed: int, lig_index: int, phase: int, gen: int, n_idx: int,
+                n_comp: int) -> np.ndarray:
+    out = np.empty((n_idx, n_comp), np.float64)
+    lib().or_rng_normals(int(seed), int(lig_index), int(phase), int(gen), int(n_idx),
+                         int(n_comp), out.ctypes.data)
     return out
 
 

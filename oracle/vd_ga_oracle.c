@@ -15,8 +15,12 @@
  *                                   = per-generation best
  * Only the random stream differs from the reference (numpy's sequential
  * Generator cannot run data-parallel): every draw is addressed by counter
- * through csrc/vd_rng.h, the same header the CUDA GA kernel compiles, so the
- * device GA and this oracle consume identical numbers.
+ * through or_rng.c, the oracle's own restatement of the counter map and
+ * transforms.  No product source is compiled in here:
+ * the device GA is checked against this independent stream bit for bit.
+ *
+ * Arithmetic: the reference's numpy float64 element-wise operations are
+ * single IEEE operations; -ffp-contract=off keeps them unfused.
  */
 #include <math.h>
 #include <stdint.h>
@@ -27,7 +31,7 @@
 #endif
 
 #include "vd_oracle.h"
-#include "vd_rng.h"
+#include "or_rng.h"
 
 typedef struct {
     int pop, generations, tournament, elitism;
@@ -44,29 +48,31 @@ void or_init_population(const or_ga_params *P, int n_torsions, uint64_t k0, uint
 {
     const int G = 7 + n_torsions;
     const double PI = 3.141592653589793;
+    const or_rng_key key = {k0, k1};
     for (int i = 0; i < P->pop; ++i) {
         double *g = pop + (size_t)i * G;
+        /* t = lo + (hi - lo) * U (ga.py:101-102); slots 0-2 of the init uniforms */
         for (int a = 0; a < 3; ++a) {
-            double u = vd_u01(vd_word(a, i, 0, VD_PH_INIT_U, k0, k1));
-            g[a] = VD_DADD(P->lo[a], VD_DMUL(VD_DSUB(P->hi[a], P->lo[a]), u));
+            double u = or_rng_uniform(or_rng_word(&key, OR_PH_INIT_U, 0, i, a));
+            g[a] = P->lo[a] + (P->hi[a] - P->lo[a]) * u;
         }
+        /* q = N(0,1)^4 / |q| (ga.py:103-106) */
         double q[4];
-        for (int c = 0; c < 4; ++c) q[c] = vd_normal(c, i, 0, VD_PH_INIT_N, k0, k1);
-        double n = VD_DSQRT(VD_DADD(VD_DADD(VD_DADD(VD_DMUL(q[0], q[0]), VD_DMUL(q[1], q[1])),
-                                            VD_DMUL(q[2], q[2])), VD_DMUL(q[3], q[3])));
+        for (int c = 0; c < 4; ++c) q[c] = or_rng_normal(&key, OR_PH_INIT_N, 0, i, c);
+        double n = sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
         if (n < 1e-12) { q[0] = 1.0; q[1] = q[2] = q[3] = 0.0; n = 1.0; }
-        for (int c = 0; c < 4; ++c) g[3 + c] = VD_DDIV(q[c], n);
+        for (int c = 0; c < 4; ++c) g[3 + c] = q[c] / n;
+        /* theta = -pi + 2 pi U (ga.py:107-108); slots 4.. */
         for (int t = 0; t < n_torsions; ++t) {
-            double u = vd_u01(vd_word(4 + t, i, 0, VD_PH_INIT_U, k0, k1));
-            g[7 + t] = VD_DADD(-PI, VD_DMUL(2.0 * PI, u));
+            double u = or_rng_uniform(or_rng_word(&key, OR_PH_INIT_U, 0, i, 4 + t));
+            g[7 + t] = -PI + (2.0 * PI) * u;
         }
     }
 }
 
 static double quat_norm(const double *q)
 {
-    return VD_DSQRT(VD_DADD(VD_DADD(VD_DADD(VD_DMUL(q[0], q[0]), VD_DMUL(q[1], q[1])),
-                                    VD_DMUL(q[2], q[2])), VD_DMUL(q[3], q[3])));
+    return sqrt(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
 }
 
 /* One child of generation `gen` (ga.py:139-174 for a single row). */
@@ -74,34 +80,36 @@ void or_breed_child(const or_ga_params *P, int G, const double *cur, const doubl
                     int gen, int c, uint64_t k0, uint64_t k1, double *child, or_ga_counts *cnt)
 {
     const int k = P->tournament;
+    const or_rng_key key = {k0, k1};
+#define BREED_WORD(slot) or_rng_word(&key, OR_PH_BREED_U, gen, c, (slot))
     int win[2];
     for (int r = 0; r < 2; ++r) {
         int best = -1;
         for (int j = 0; j < k; ++j) {
-            int idx = (int)vd_below(vd_word(r * k + j, c, gen, VD_PH_BREED_U, k0, k1),
-                                    (uint64_t)P->pop);
+            int idx = (int)or_rng_below(BREED_WORD(r * k + j), (uint64_t)P->pop);
             if (best < 0 || fit[idx] < fit[best]) best = idx;
         }
         win[r] = best;
     }
     const double *p1 = cur + (size_t)win[0] * G, *p2 = cur + (size_t)win[1] * G;
-    int do_cx = vd_u01(vd_word(2 * k, c, gen, VD_PH_BREED_U, k0, k1)) < P->cx_rate;
-    int a = (int)vd_below(vd_word(2 * k + 1, c, gen, VD_PH_BREED_U, k0, k1), (uint64_t)G + 1);
-    int b = (int)vd_below(vd_word(2 * k + 2, c, gen, VD_PH_BREED_U, k0, k1), (uint64_t)G + 1);
+    int do_cx = or_rng_uniform(BREED_WORD(2 * k)) < P->cx_rate;
+    int a = (int)or_rng_below(BREED_WORD(2 * k + 1), (uint64_t)G + 1);
+    int b = (int)or_rng_below(BREED_WORD(2 * k + 2), (uint64_t)G + 1);
     int c_lo = a < b ? a : b, c_hi = a < b ? b : a;
     int mut_rot = 0;
     for (int g = 0; g < G; ++g) {
         double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
-        int mut = vd_u01(vd_word(2 * k + 3 + g, c, gen, VD_PH_BREED_U, k0, k1)) < P->mut_rate;
+        int mut = or_rng_uniform(BREED_WORD(2 * k + 3 + g)) < P->mut_rate;
         double noise = 0.0;
         if (mut) {
             double sig = g < 3 ? P->sigma_t : (g < 7 ? P->sigma_r : P->sigma_tor);
-            noise = VD_DMUL(vd_normal(g, c, gen, VD_PH_BREED_N, k0, k1), sig);
+            noise = or_rng_normal(&key, OR_PH_BREED_N, gen, c, g) * sig;
             if (g >= 3 && g < 7) mut_rot = 1;
             if (cnt) cnt->gene_mutations++;
         }
-        child[g] = VD_DADD(v, noise);
+        child[g] = v + noise;
     }
+#undef BREED_WORD
     double n = quat_norm(child + 3);
     int bad = n < 1e-9;
     if (bad) {
@@ -109,7 +117,7 @@ void or_breed_child(const or_ga_params *P, int G, const double *cur, const doubl
         n = quat_norm(child + 3);
     }
     if (mut_rot || bad)
-        for (int q = 3; q < 7; ++q) child[q] = VD_DDIV(child[q], n);
+        for (int q = 3; q < 7; ++q) child[q] = child[q] / n;
     if (cnt) {
         cnt->children++;
         cnt->crossovers += do_cx;
@@ -214,13 +222,15 @@ int or_dock_many(const or_ligand *ligs, int n_ligs, const or_ga_params *P, uint6
 void or_philox_block(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3, uint64_t k0,
                      uint64_t k1, uint64_t *out)
 {
-    vd_u64x4 w = vd_philox4x64_10(c0, c1, c2, c3, k0, k1);
-    memcpy(out, w.v, sizeof w.v);
+    const uint64_t ctr[4] = {c0, c1, c2, c3}, key[2] = {k0, k1};
+    or_philox(ctr, key, out);
 }
 
-double or_log(double x) { return vd_log(x); }
-double or_cos2pi(double u) { return vd_cos2pi(u); }
+double or_log(double x) { return or_rng_ln(x); }
+double or_cos2pi(double u) { return or_rng_cos_2pi(u); }
+/* normal of block (c0 = component, c1 = individual, c2 = generation, c3 = phase) */
 double or_normal(uint64_t c0, uint64_t c1, uint64_t c2, uint64_t c3, uint64_t k0, uint64_t k1)
 {
-    return vd_normal(c0, c1, c2, c3, k0, k1);
+    const or_rng_key key = {k0, k1};
+    return or_rng_normal(&key, (int)c3, (int64_t)c2, (int64_t)c1, (int64_t)c0);
 }

@@ -62,10 +62,11 @@ class VdGaParams(C.Structure):
 
 EXPORTS = (
     "vd_abi_version", "vd_last_error", "vd_device_count", "vd_init", "vd_grid_create",
-    "vd_grid_build", "vd_grid_n_maps", "vd_grid_download", "vd_grid_destroy",
+    "vd_grid_build", "vd_grid_n_maps", "vd_grid_layout", "vd_grid_download", "vd_grid_destroy",
     "vd_ligands_create", "vd_ligands_n_torsions", "vd_ligands_destroy", "vd_score_genes",
     "vd_score_poses", "vd_pose_genes", "vd_dock_batch", "vd_last_launch_count",
     "vd_prepare_count", "vd_prepare_fill", "vd_synth_count", "vd_synth_fill",
+    "vd_debug_rng", "vd_debug_ga_init", "vd_debug_ga_breed", "vd_debug_pose_genes",
 )
 
 
@@ -84,6 +85,7 @@ def load_library(path: Path = LIB_PATH):
     L.vd_grid_build.argtypes = [vp, vp, vp, i32, vp, i32, vp, i32, vp, C.c_double, i32, i32,
                                 i32, vp, C.c_double, vp]
     L.vd_grid_n_maps.argtypes = [vp]
+    L.vd_grid_layout.argtypes = [vp]
     L.vd_grid_download.argtypes = [vp, vp]
     L.vd_grid_destroy.argtypes = [vp]
     L.vd_ligands_create.argtypes = [vp, vp]
@@ -99,6 +101,10 @@ def load_library(path: Path = LIB_PATH):
     L.vd_prepare_fill.argtypes = [i32] + [vp] * 8 + [vp, i32, vp, vp, C.c_double] + [vp] * 16
     L.vd_synth_count.argtypes = [u64, i64, i32, i32, i32, C.c_double, i32, i32, vp, vp]
     L.vd_synth_fill.argtypes = [u64, i64, i32, i32, i32, C.c_double, i32, i32, vp, i32] + [vp] * 7
+    L.vd_debug_rng.argtypes = [i32, u64, u64, i32, i64, i64, i32, vp]
+    L.vd_debug_ga_init.argtypes = [vp, i32, u64, u64, vp]
+    L.vd_debug_ga_breed.argtypes = [vp, i32, vp, vp, i32, u64, u64, vp]
+    L.vd_debug_pose_genes.argtypes = [vp, i32, vp, i64, i32, vp]
     return L
 
 
@@ -184,6 +190,13 @@ class DeviceGrid:
         self.dims = tuple(dims)
         self.lo, self.hi, self.spacing = lo, hi, spacing
         self.labels = labels
+
+    LAYOUTS = {0: "plain", 1: "brick", 2: "zpair"}
+
+    @property
+    def layout(self) -> str:
+        """Gather layout chosen at creation: "plain", "brick" (yz-bricks) or "zpair"."""
+        return self.LAYOUTS[int(lib().vd_grid_layout(self.handle))]
 
     def download(self) -> np.ndarray:
         out = np.empty((self.n_maps,) + self.dims, np.float32)
@@ -365,3 +378,47 @@ def dock_batch(grid: DeviceGrid, ligs: LigandSet, first: int, count: int, params
                               ptr_of(best_total), ptr_of(best_inter), ptr_of(best_intra),
                               ptr_of(best_genes), int(best_genes.shape[1]), ptr_of(trace),
                               ptr_of(n_evals), stream), "vd_dock_batch")
+
+
+# ---- test probes (vd_debug_*): the GA's device draws / operators on chosen inputs ----
+def debug_rng_words(seed: int, lig_index: int, phase: int, gen: int, n_idx: int,
+                    n_slot: int) -> np.ndarray:
+    out = np.empty((n_idx, n_slot), np.uint64)
+    check(lib().vd_debug_rng(0, int(seed), int(lig_index), int(phase), int(gen), int(n_idx),
+                             int(n_slot), out.ctypes.data), "vd_debug_rng")
+    return out
+
+
+def debug_rng_normals(seed: int, lig_index: int, phase: int, gen: int, n_idx: int,
+                      n_comp: int) -> np.ndarray:
+    out = np.empty((n_idx, n_comp), np.float64)
+    check(lib().vd_debug_rng(1, int(seed), int(lig_index), int(phase), int(gen), int(n_idx),
+                             int(n_comp), out.ctypes.data), "vd_debug_rng")
+    return out
+
+
+def debug_ga_init(params: VdGaParams, n_torsions: int, seed: int, lig_index: int) -> np.ndarray:
+    out = np.empty((params.pop, 7 + n_torsions), np.float64)
+    check(lib().vd_debug_ga_init(C.byref(params), int(n_torsions), int(seed), int(lig_index),
+                                 out.ctypes.data), "vd_debug_ga_init")
+    return out
+
+
+def debug_ga_breed(params: VdGaParams, n_torsions: int, cur: np.ndarray, fitness: np.ndarray,
+                   gen: int, seed: int, lig_index: int) -> np.ndarray:
+    cur = np.ascontiguousarray(cur, np.float64)
+    fit = np.ascontiguousarray(fitness, np.float32)
+    out = np.empty((params.pop - params.elitism, 7 + n_torsions), np.float64)
+    check(lib().vd_debug_ga_breed(C.byref(params), int(n_torsions), cur.ctypes.data,
+                                  fit.ctypes.data, int(gen), int(seed), int(lig_index),
+                                  out.ctypes.data), "vd_debug_ga_breed")
+    return out
+
+
+def debug_pose_genes(ligs: LigandSet, lig: int, genes: np.ndarray, tpp: int) -> np.ndarray:
+    """(P, 3, N) poses from the fast score kernel's TPP = 4/8 pose stage."""
+    g = np.ascontiguousarray(genes, np.float64)
+    out = np.empty((g.shape[0], 3, int(ligs.n_atoms[lig])), np.float32)
+    check(lib().vd_debug_pose_genes(ligs.handle, int(lig), g.ctypes.data, int(g.shape[0]),
+                                    int(tpp), out.ctypes.data), "vd_debug_pose_genes")
+    return out

@@ -32,7 +32,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
                          const double *genes, const float *poses, int64_t P, int ngenes,
                          double *inter, double *intra, float *total, cudaStream_t st);
 cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ngenes, float *out,
-                        cudaStream_t st);
+                        cudaStream_t st, int tpp_force);
 }  // namespace vd
 
 namespace vdi {
@@ -316,6 +316,12 @@ int vd_grid_create(const float *maps, int n_maps, int nx, int ny, int nz, const 
 }
 
 int vd_grid_n_maps(const vd_grid *g) { return g ? g->n_maps : -1; }
+
+int vd_grid_layout(const vd_grid *g)
+{
+    if (!g) return -1;
+    return g->d_yz ? (g->zpair ? VD_LAYOUT_ZPAIR : VD_LAYOUT_BRICK) : VD_LAYOUT_PLAIN;
+}
 
 int vd_grid_download(const vd_grid *g, float *out)
 {
@@ -613,8 +619,8 @@ int vd_score_poses(const vd_grid *g, const vd_ligands *s, int lig, const float *
     return score_common(g, s, lig, poses, false, P, inter, intra, nullptr, mode, stream);
 }
 
-int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, float *poses,
-                  void *stream)
+static int pose_common(const vd_ligands *s, int lig, const double *genes, int64_t P, float *poses,
+                       void *stream, int tpp)
 {
     if (!s || lig < 0 || lig >= s->n_ligands) {
         set_error("vd_pose_genes: bad ligand handle or index");
@@ -632,7 +638,7 @@ int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, 
         VD_CK(cudaMemcpyAsync((void *)dg, genes, P * ngenes * sizeof(double), cudaMemcpyHostToDevice, st));
     }
     if (!pout) VD_CK(cudaMallocAsync((void **)&dp, P * 3 * L.n_atoms * sizeof(float), st));
-    VD_CK(vd::launch_pose(L, dg, P, ngenes, dp, st));
+    VD_CK(vd::launch_pose(L, dg, P, ngenes, dp, st, tpp));
     if (!pout) {
         VD_CK(cudaMemcpyAsync(poses, dp, P * 3 * L.n_atoms * sizeof(float), cudaMemcpyDeviceToHost, st));
         VD_CK(cudaFreeAsync(dp, st));
@@ -640,6 +646,22 @@ int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, 
     if (!gin) VD_CK(cudaFreeAsync((void *)dg, st));
     if (!pout) VD_CK(cudaStreamSynchronize(st));
     return 0;
+}
+
+int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, float *poses,
+                  void *stream)
+{
+    return pose_common(s, lig, genes, P, poses, stream, 0);
+}
+
+int vd_debug_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, int tpp,
+                        float *poses)
+{
+    if (tpp != 4 && tpp != 8) {
+        set_error("vd_debug_pose_genes: tpp must be 4 or 8");
+        return -1;
+    }
+    return pose_common(s, lig, genes, P, poses, nullptr, tpp);
 }
 
 }  // extern "C"

@@ -371,9 +371,120 @@ int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes, bool packed)
     return 0;
 }
 
+/* ---- test probes: the GA's own device draw and operator code on chosen inputs ---- */
+__global__ void rng_probe_kernel(int kind, uint64_t k0, uint64_t k1, int phase, int64_t gen,
+                                 int64_t n_idx, int n_slot, void *out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_idx) return;
+    if (kind == 0) {
+        vd_words W = vd_words_at(i, gen, phase, k0, k1);
+        uint64_t *o = static_cast<uint64_t *>(out) + i * n_slot;
+        for (int s = 0; s < n_slot; ++s) o[s] = vd_words_get(&W, s);
+    } else {
+        double *o = static_cast<double *>(out) + i * n_slot;
+        for (int s = 0; s < n_slot; ++s) o[s] = vd_normal(s, i, gen, phase, k0, k1);
+    }
+}
+
+__global__ void ga_init_probe_kernel(GaDev P, int T, uint64_t k0, uint64_t k1, double *out)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P.pop) init_individual(P, T, i, k0, k1, out + (size_t)i * (7 + T));
+}
+
+__global__ void ga_breed_probe_kernel(GaDev P, int T, const double *cur, const float *fit, int gen,
+                                      uint64_t k0, uint64_t k1, double *out)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int G = 7 + T;
+    if (c < P.pop - P.elitism) breed_child(P, G, cur, fit, gen, c, k0, k1, out + (size_t)c * G);
+}
+
 }  // namespace vd
 
 using vdi::set_error;
+
+static vd::GaDev ga_dev(const vd_ga_params *p)
+{
+    vd::GaDev P;
+    P.pop = p->pop; P.generations = p->generations; P.tournament = p->tournament;
+    P.elitism = p->elitism;
+    P.cx_rate = p->cx_rate; P.mut_rate = p->mut_rate;
+    P.sigma_t = p->sigma_t; P.sigma_r = p->sigma_r; P.sigma_tor = p->sigma_tor;
+    for (int k = 0; k < 3; ++k) { P.lo[k] = p->lo[k]; P.hi[k] = p->hi[k]; }
+    return P;
+}
+
+extern "C" int vd_debug_rng(int kind, uint64_t seed, uint64_t lig_index, int phase, int64_t gen,
+                            int64_t n_idx, int n_slot, void *out)
+{
+    if ((kind != 0 && kind != 1) || n_idx < 0 || n_slot < 1 || !out) {
+        set_error("vd_debug_rng: bad arguments");
+        return -1;
+    }
+    if (n_idx == 0) return 0;
+    const size_t bytes = 8u * (size_t)n_idx * n_slot;
+    void *d = nullptr;
+    VD_CK(cudaMalloc(&d, bytes));
+    vd::rng_probe_kernel<<<(unsigned)((n_idx + 127) / 128), 128>>>(kind, seed, lig_index, phase, gen,
+                                                                    n_idx, n_slot, d);
+    ++vdi::g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    VD_CK(e);
+    return 0;
+}
+
+extern "C" int vd_debug_ga_init(const vd_ga_params *p, int n_torsions, uint64_t seed,
+                                uint64_t lig_index, double *out)
+{
+    if (!p || p->pop < 1 || n_torsions < 0 || !out) {
+        set_error("vd_debug_ga_init: bad arguments");
+        return -1;
+    }
+    const size_t bytes = sizeof(double) * (size_t)p->pop * (7 + n_torsions);
+    double *d = nullptr;
+    VD_CK(cudaMalloc((void **)&d, bytes));
+    vd::ga_init_probe_kernel<<<(p->pop + 127) / 128, 128>>>(ga_dev(p), n_torsions, seed, lig_index, d);
+    ++vdi::g_launches;
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, bytes, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    VD_CK(e);
+    return 0;
+}
+
+extern "C" int vd_debug_ga_breed(const vd_ga_params *p, int n_torsions, const double *cur,
+                                 const float *fitness, int gen, uint64_t seed, uint64_t lig_index,
+                                 double *children)
+{
+    if (!p || p->pop < 2 || p->elitism < 0 || p->elitism >= p->pop || p->tournament < 1 ||
+        n_torsions < 0 || !cur || !fitness || !children) {
+        set_error("vd_debug_ga_breed: bad arguments");
+        return -1;
+    }
+    const int G = 7 + n_torsions, nc = p->pop - p->elitism;
+    const size_t pop_bytes = sizeof(double) * (size_t)p->pop * G;
+    double *d_cur = nullptr, *d_out = nullptr;
+    float *d_fit = nullptr;
+    VD_CK(cudaMalloc((void **)&d_cur, pop_bytes));
+    VD_CK(cudaMalloc((void **)&d_out, sizeof(double) * (size_t)nc * G));
+    VD_CK(cudaMalloc((void **)&d_fit, sizeof(float) * (size_t)p->pop));
+    cudaError_t e = cudaMemcpy(d_cur, cur, pop_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(d_fit, fitness, sizeof(float) * p->pop, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        vd::ga_breed_probe_kernel<<<(nc + 127) / 128, 128>>>(ga_dev(p), n_torsions, d_cur, d_fit, gen,
+                                                              seed, lig_index, d_out);
+        ++vdi::g_launches;
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(children, d_out, sizeof(double) * (size_t)nc * G, cudaMemcpyDeviceToHost);
+    cudaFree(d_cur); cudaFree(d_out); cudaFree(d_fit);
+    VD_CK(e);
+    return 0;
+}
 
 extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, int count,
                              const vd_ga_params *p, uint64_t seed, int64_t lig_index_base,
@@ -493,12 +604,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         order.insert(order.end(), v.begin(), v.end());
         launches.push_back(L);
     }
-    vd::GaDev P;
-    P.pop = p->pop; P.generations = p->generations; P.tournament = p->tournament;
-    P.elitism = p->elitism;
-    P.cx_rate = p->cx_rate; P.mut_rate = p->mut_rate;
-    P.sigma_t = p->sigma_t; P.sigma_r = p->sigma_r; P.sigma_tor = p->sigma_tor;
-    for (int k = 0; k < 3; ++k) { P.lo[k] = p->lo[k]; P.hi[k] = p->hi[k]; }
+    const vd::GaDev P = ga_dev(p);
 
     const bool dev_out = vdi::is_device_ptr(best_total);
     vd::LigView *d_views = nullptr;

@@ -78,22 +78,27 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     }
 }
 
-template <int NPP>
-__global__ void __launch_bounds__(NPP) pose_kernel(LigView Lg, const double *__restrict__ genes,
-                                                   int64_t P, int ngenes, SmemLayout lay,
-                                                   float one, float *__restrict__ out)
+/* Poses only: the score kernel's pose stage (build_pose2<NPP, TPP>, the same shared tile,
+ * scratch and sub-thread split) with the tile written out instead of scored.  TPP = 1 serves
+ * vd_pose_genes; TPP = 4 / 8 are the fast score kernel's shapes (vd_debug_pose_genes). */
+template <int NPP, int TPP>
+__global__ void __launch_bounds__(NPP *TPP) pose_kernel(LigView Lg, const double *__restrict__ genes,
+                                                        int64_t P, int ngenes, SmemLayout lay,
+                                                        float one, float *__restrict__ out)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int pp = threadIdx.x;
+    const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
     const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
                                      lay.topo_frag);
     __syncthreads();
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
     const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;
-    build_pose2<NPP, 1>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, 0, nullptr, one);
+    build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
+                          TPP > 1 ? reinterpret_cast<float *>(smem + lay.scratch) + pp : nullptr, one);
+    if (TPP > 1) __syncthreads();
     const int n = L.n_atoms;
-    for (int i = 0; i < n; ++i)
+    for (int i = sub; i < n; i += TPP)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const float2 v = VD_S2(i, c);
@@ -240,22 +245,35 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
     return cudaErrorInvalidConfiguration;
 }
 
+/* tpp 0: the TPP = 1 pose path of vd_pose_genes; tpp > 0: the fast score kernel's pose-tile
+ * shape for that TPP (its NPP from pick_shape), for the bitwise pose test */
 cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ngenes, float *out,
-                        cudaStream_t st)
+                        cudaStream_t st, int tpp_force)
 {
     int npp, tpp;
-    if (pick_shape(L.n_atoms, 0, L.n_torsions, true, &npp, &tpp)) return cudaErrorInvalidValue;
+    if (tpp_force > 0) {
+        if (pick_shape(L.n_atoms, L.n_pairs, L.n_torsions, false, &npp, &tpp)) return cudaErrorInvalidValue;
+        tpp = tpp_force;
+        const unsigned b = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, tpp, 0, 0).bytes;
+        if (b > 200u * 1024u) return cudaErrorInvalidValue;
+    } else if (pick_shape(L.n_atoms, 0, L.n_torsions, true, &npp, &tpp)) {
+        return cudaErrorInvalidValue;
+    }
     if (P <= 0) return cudaSuccess;
-    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, 1, 0, 0);
+    const SmemLayout lay = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, tpp, 0, 0);
     const size_t smem = lay.bytes;
     const int64_t blocks = (P + 2 * npp - 1) / (2 * npp);
-    cudaError_t e;
-#define VD_P(N)                                                                                   \
-    if (npp == N) {                                                                               \
-        e = vdi::raise_smem_limit((const void *)pose_kernel<N>, (unsigned)smem);                    \
-        if (e == cudaSuccess) pose_kernel<N><<<(unsigned)blocks, N, smem, st>>>(L, genes, P, ngenes, lay, 1.0f /* run-time: see xadd2 */, out); \
+    cudaError_t e = cudaErrorInvalidConfiguration;
+#define VD_P(N, T)                                                                                \
+    if (npp == N && tpp == T) {                                                                   \
+        e = vdi::raise_smem_limit((const void *)pose_kernel<N, T>, (unsigned)smem);                \
+        if (e == cudaSuccess)                                                                     \
+            pose_kernel<N, T><<<(unsigned)blocks, N * T, smem, st>>>(L, genes, P, ngenes, lay,    \
+                                                                     1.0f /* run-time: see xadd2 */, out); \
     }
-    VD_P(64) else VD_P(32) else VD_P(16) else return cudaErrorInvalidConfiguration;
+    VD_P(64, 1) else VD_P(32, 1) else VD_P(16, 1)
+    else VD_P(64, 4) else VD_P(32, 4) else VD_P(16, 4)
+    else VD_P(64, 8) else VD_P(32, 8) else VD_P(16, 8)
 #undef VD_P
     if (e != cudaSuccess) return e;
     ++vdi::g_launches;

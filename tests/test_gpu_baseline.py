@@ -1,0 +1,185 @@
+"""Parity on the BASELINE.json workloads themselves: the cfg0 48^3, cfg1 80^3, cfg2 64^3
+and cfg4 126^3 grids built on the device from the configs' synthetic receptors, the
+configs' ligand distributions, and the GA at the configs' population sizes.
+
+* per-pose energies (inter, intra, total) of 16k random poses per config vs the
+  oracle on the same maps, in both modes, on the gather layout each grid gets
+  (cfg1 z-pairs, cfg2 yz-bricks, cfg4 plain): vd/scoring/simd.py:157-240,
+  pkg/tests/test_scoring.py:250-267;
+* the fast score kernel's TPP = 4 / 8 pose stage, bit for bit (vd/pose.py:137-205);
+* generation 0 of the fast GA kernel (its own scoring path: shared reciprocal,
+  pipelined gathers) on 512 cfg2 and 32 cfg4 ligands vs the oracle GA with the
+  same keys, and every returned best genotype re-scored by the oracle
+  (vd/ga.py:180-235).
+Tolerance (north star): |d| <= 1e-3 kcal/mol or |d|/|E_ref| <= 1e-4.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle, parity
+
+pytestmark = pytest.mark.gpu
+
+LAYOUT = {0: "zpair", 1: "zpair", 2: "brick", 4: "plain"}  # what vd_grid_create picks
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2509_12232_b200 import _abi
+
+    _abi.ensure_device(0)
+    return _abi
+
+
+_GRIDS = {}
+
+
+def workload_grid(cfg):
+    """(GridMapSet with host maps, DeviceGrid, host stack in device label order)."""
+    if cfg not in _GRIDS:
+        from paper_2509_12232_b200 import gridmaps, synth
+        from paper_2509_12232_b200.backend import CudaBackend
+
+        spec = synth.config_grid_spec(cfg)
+        gset = gridmaps.build_grid_maps(synth.config_protein(cfg), spec,
+                                        synth.CONFIGS[cfg].probe_types)
+        b = CudaBackend(mode="fast", device=0)
+        grid = b._grid_for_set(gset)
+        stack = np.stack([gset.maps[l] for l in grid.labels]).astype(np.float32)
+        _GRIDS[cfg] = (gset, grid, stack, b)
+    return _GRIDS[cfg]
+
+
+def batch_case(cfg, first, count):
+    from paper_2509_12232_b200 import hostprep
+
+    gset, grid, stack, _ = workload_grid(cfg)
+    batch = hostprep.TopologyBatch.synth(cfg, first, count)
+    arrays = hostprep.prepare_batch(batch, grid.labels)
+    return arrays, hostprep.ligand_set(arrays), oracle.ligands_from_arrays(arrays, stack, gset.spec)
+
+
+def _check(got, want, what):
+    ok = parity.within_tol(got, want)
+    assert ok.all(), (what, int((~ok).sum()), np.asarray(got)[~ok][:4], np.asarray(want)[~ok][:4])
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+@pytest.mark.parametrize("cfg", [0, 1])
+def test_single_ligand_configs_16k_poses(dev, cfg, mode):
+    from paper_2509_12232_b200 import synth
+    from paper_2509_12232_b200.backend import CudaBackend
+    from paper_2509_12232_b200.context import prepare_context
+
+    gset, grid, _, _ = workload_grid(cfg)
+    assert grid.layout == LAYOUT[cfg]
+    ctx = prepare_context(synth.config_ligand(cfg, 0), gset)
+    genes = synth.random_genes(100 + cfg, 16384, ctx.n_torsions, gset.spec.origin, gset.spec.upper)
+    e, a, t = CudaBackend(mode=mode, device=0).score_population_arrays(genes, ctx)
+    we, wa, wt = oracle.dock_population(oracle.Ligand(ctx), genes, n_threads=0)
+    if mode == "exact":
+        assert np.array_equal(e, we) and np.array_equal(a, wa) and np.array_equal(t, wt)
+    _check(e, we, "inter")
+    _check(a, wa, "intra")
+    _check(t, wt, "total")
+
+
+@pytest.mark.parametrize("mode", ["fast", "exact"])
+@pytest.mark.parametrize("cfg,count,per", [(2, 8, 2048), (4, 2, 8192)])
+def test_batch_configs_16k_poses(dev, cfg, count, per, mode):
+    from paper_2509_12232_b200 import synth
+
+    gset, grid, _, _ = workload_grid(cfg)
+    assert grid.layout == LAYOUT[cfg]
+    arrays, lset, ligs = batch_case(cfg, 37, count)
+    m = dev.MODE_FAST if mode == "fast" else dev.MODE_EXACT
+    for l in range(count):
+        T = int(lset.n_torsions[l])
+        genes = synth.random_genes(7 * l + cfg, per, T, gset.spec.origin, gset.spec.upper)
+        e, a, t = np.empty(per), np.empty(per), np.empty(per, np.float32)
+        dev.score_genes(grid, lset, l, genes, e, a, t, mode=m)
+        we, wa, wt = oracle.dock_population(ligs[l], genes, n_threads=0)
+        if mode == "exact":
+            assert np.array_equal(e, we) and np.array_equal(a, wa) and np.array_equal(t, wt)
+        _check(e, we, f"inter lig {l}")
+        _check(a, wa, f"intra lig {l}")
+        _check(t, wt, f"total lig {l}")
+
+
+@pytest.mark.parametrize("cfg,count", [(1, 1), (2, 6), (4, 2)])
+@pytest.mark.parametrize("tpp", [4, 8])
+def test_score_kernel_pose_stage_bitwise(dev, cfg, count, tpp):
+    """The TPP = 4/8 pose path every fast launch uses (spread sincos, sub-shared
+    matrices, barrier-ordered torsion chain, packed fma(x, one, y)) vs the oracle's
+    reference-sequence poses, bit for bit."""
+    from paper_2509_12232_b200 import synth
+    from paper_2509_12232_b200.context import prepare_context
+
+    gset, grid, stack, b = workload_grid(cfg)
+    if cfg == 1:
+        ctx = prepare_context(synth.config_ligand(1, 0), gset)
+        _, lset = b.prepared(ctx)
+        ligs = [oracle.Ligand(ctx)]
+    else:
+        _, lset, ligs = batch_case(cfg, 5, count)
+    for l in range(count):
+        T = int(lset.n_torsions[l])
+        genes = synth.random_genes(31 + l, 4099, T, gset.spec.origin, gset.spec.upper)
+        genes[:5, 3:7] *= np.array([[1e-3], [7.0], [-2.5], [1e3], [0.2]])  # non-unit quaternions
+        got = dev.debug_pose_genes(lset, l, genes, tpp)
+        want = oracle.pose_population(ligs[l], genes)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (cfg, l, tpp)
+
+
+def _ga(pop, gens, spec):
+    from paper_2509_12232_b200.ga import GaConfig
+
+    return GaConfig(population_size=pop, generations=gens,
+                    translation_bounds=(spec.origin, spec.upper))
+
+
+@pytest.mark.parametrize("cfg,count,pop", [(2, 512, 256), (4, 32, 512)])
+def test_fast_ga_generation0_matches_oracle(dev, cfg, count, pop):
+    """generations = 0: the fast GA kernel scores the initial population, which is drawn
+    bit-identically to the oracle's (tests/test_gpu_rng.py), so its best must be the
+    oracle's best within tolerance on every ligand -- a direct check of the GA kernel's
+    own scoring path.  The returned best genotype must be one of the oracle's initial
+    individuals, and its oracle energies must equal what the device reported."""
+    from paper_2509_12232_b200.ga import _run
+
+    gset, grid, _, _ = workload_grid(cfg)
+    arrays, lset, ligs = batch_case(cfg, 0, count)
+    ga = _ga(pop, 0, gset.spec)
+    gmax = 7 + int(lset.n_torsions.max())
+    base = 1000
+    bt, be, ba, bg, tr, ne = _run(grid, lset, 0, count, ga, 0, base, dev.MODE_FAST, gmax)
+    params = oracle.ga_params(ga, gset.spec.origin, gset.spec.upper)
+    og, obt, obe, oba, one = oracle.dock_many(ligs, params, 0, base, n_threads=0)
+    _check(bt, obt, "generation-0 best_total")
+    assert np.array_equal(ne, one) and np.all(ne == pop)
+    assert np.array_equal(tr[:, 0], bt)
+    rs = parity.rescore_summary(ligs, bt, be, ba, bg)
+    assert rs["best_rescored_within_tol"] == count, rs
+    for l in range(0, count, max(1, count // 16)):
+        G = 7 + ligs[l].n_torsions
+        init = oracle.init_population(params, ligs[l].n_torsions, (0, base + l))
+        assert (init == bg[l, :G]).all(axis=1).any(), l
+
+
+@pytest.mark.parametrize("cfg,count,pop,gens", [(2, 64, 256, 200), (4, 4, 512, 300)])
+def test_fast_ga_full_length_best_is_rescored_exactly(dev, cfg, count, pop, gens):
+    """BASELINE GA lengths: every best the fast GA returns after pop x gens is the
+    oracle's energy of the returned genotype (within tolerance)."""
+    from paper_2509_12232_b200.ga import _run
+
+    gset, grid, _, _ = workload_grid(cfg)
+    arrays, lset, ligs = batch_case(cfg, 200, count)
+    gmax = 7 + int(lset.n_torsions.max())
+    bt, be, ba, bg, tr, ne = _run(grid, lset, 0, count, _ga(pop, gens, gset.spec), 0, 200,
+                                  dev.MODE_FAST, gmax)
+    assert np.array_equal(tr.min(axis=1), bt)  # trace = per-generation best (vd/ga.py:222)
+    rs = parity.rescore_summary(ligs, bt, be, ba, bg)
+    assert rs["best_rescored_within_tol"] == count, rs

@@ -4,6 +4,7 @@ pkg/tests/test_ga.py properties), RNG transforms, MUGD I/O, mirror validation.""
 
 from __future__ import annotations
 
+import ctypes
 import io
 import math
 import os
@@ -214,6 +215,52 @@ def test_rng_transcendentals_accurate():
         assert abs(L.or_cos2pi(float(u)) - math.cos(2 * math.pi * u)) <= 1e-15
     z = np.array([L.or_normal(c, 1, 2, 4, 7, 3) for c in range(20000)])
     assert abs(z.mean()) < 0.05 and abs(z.std() - 1.0) < 0.03
+
+
+def _numpy_philox_at(key, counter):
+    """numpy's Philox positioned so its next block is `counter` (numpy bumps the
+    counter before each block)."""
+    prev = list(counter)
+    for w in range(4):
+        if prev[w] > 0:
+            prev[w] -= 1
+            break
+        prev[w] = 2**64 - 1
+    return np.random.Philox(key=np.array(key, np.uint64), counter=np.array(prev, np.uint64))
+
+
+@pytest.mark.parametrize("seed,lig,phase,gen", [(0, 0, 1, 0), (2**63 + 11, 99_999, 3, 199),
+                                                (7, 12_345, 4, 57)])
+def test_oracle_stream_pinned_to_numpy(seed, lig, phase, gen):
+    """The oracle's counter map, uniform and integer transforms against numpy itself:
+    word (idx, slot) = Philox(key=(seed, lig)) block (slot//4, idx, gen, phase) [slot%4];
+    uniform = Generator.random on that block; integer = floor(w * n / 2^64)."""
+    n_idx, n_slot = 64, 12
+    words = oracle.rng_words(seed, lig, phase, gen, n_idx, n_slot)
+    L = oracle.lib()
+    L.or_rng_uniform.restype = ctypes.c_double
+    L.or_rng_uniform.argtypes = [ctypes.c_uint64]
+    L.or_rng_below.restype = ctypes.c_uint64
+    L.or_rng_below.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+    for idx in range(0, n_idx, 7):
+        for blk in range(n_slot // 4):
+            ctr = (blk, idx, gen, phase)
+            raw = _numpy_philox_at((seed, lig), ctr).random_raw(4)
+            np.testing.assert_array_equal(words[idx, 4 * blk:4 * blk + 4], raw)
+            u = np.random.Generator(_numpy_philox_at((seed, lig), ctr)).random(4)
+            got = np.array([L.or_rng_uniform(int(w)) for w in raw])
+            np.testing.assert_array_equal(got, u)
+            for n in (2, 100, 257, 8192):
+                assert [L.or_rng_below(int(w), n) for w in raw] == [(int(w) * n) >> 64 for w in raw]
+
+
+def test_oracle_normals_distribution():
+    """1e5 Box-Muller normals of the oracle stream: N(0, 1) by Kolmogorov-Smirnov."""
+    from scipy import stats
+
+    z = oracle.rng_normals(5, 77, 4, 3, 25_000, 4).ravel()
+    assert stats.kstest(z, "norm").pvalue > 1e-3
+    assert abs(z.mean()) < 0.015 and abs(z.std() - 1.0) < 0.01
 
 
 # --- mirror validation / formats --------------------------------------------------------

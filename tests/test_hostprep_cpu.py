@@ -91,3 +91,27 @@ def test_synth_batches_valid_and_bitwise(cfg):
     g = gridmaps.GridMapSet(gridmaps.GridSpec.centered((0, 0, 0), (3, 3, 3), 1.0),
                             {l: z for l in labels})
     _compare(b, [prepare_context(t, g, table=fx.TABLE) for t in topos], labels)
+
+
+def test_oracle_ligands_from_arrays_score_like_contexts():
+    """oracle.ligands_from_arrays (the CSR set the device gets, over one shared map stack)
+    scores bit-identically to oracle.Ligand over prepare_context's per-ligand stack."""
+    from oracle import oracle
+    from paper_2509_12232_b200 import gridmaps, synth
+
+    spec = gridmaps.GridSpec.centered((0.0, 0.0, 0.0), (9, 10, 11), 1.5)
+    rng = np.random.default_rng(4)
+    labels = list(synth.CONFIGS[2].probe_types) + [chem.ELEC_LABEL, chem.DESOLV_LABEL]
+    gset = gridmaps.GridMapSet(spec, {l: rng.normal(0, 3, spec.dims).astype(np.float32)
+                                      for l in labels})
+    batch = hostprep.TopologyBatch.synth(2, 11, 5)
+    arrays = hostprep.prepare_batch(batch, labels)
+    stack = np.stack([gset.maps[l] for l in labels])
+    ligs = oracle.ligands_from_arrays(arrays, stack, spec)
+    for l in range(len(batch)):
+        ctx = prepare_context(batch.topology(l), gset)
+        genes = synth.random_genes(l, 64, ctx.n_torsions, spec.origin, spec.upper)
+        got = oracle.dock_population(ligs[l], genes)
+        want = oracle.dock_population(oracle.Ligand(ctx), genes)
+        for g, w in zip(got, want):
+            assert np.array_equal(g, w), l

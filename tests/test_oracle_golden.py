@@ -118,7 +118,7 @@ def test_philox_matches_numpy():
         key, counter, want = row[:2], row[2:6], row[6:]
         got = oracle.philox_block(counter, key)
         np.testing.assert_array_equal(got, want)
-    # Generator.random() == (raw >> 11) * 2^-53 (the uniform transform restated in vd_rng.h)
+    # Generator.random() == (raw >> 11) * 2^-53 (the uniform transform of or_rng.c and vd_rng.h)
     u = (d["random_raw"] >> np.uint64(11)).astype(np.float64) * 2.0**-53
     np.testing.assert_array_equal(u, d["random_u"])
 
