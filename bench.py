@@ -78,67 +78,88 @@ def build_inputs(device_grid: bool):
     return gset, lig, ctx, grid_s, grid_src
 
 
+def measured_peaks_file():
+    """The driver-written MEASURED_PEAKS.json (HBM copy GB/s; no FP32 or L2 figure)."""
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except (OSError, ValueError):
+        return {}
+
+
 def measure_peaks(grid_n=80, n_types=7):
-    """Live roofline denominators (tools/peaks.cu): FFMA2 TFLOP/s; the score kernel's own
-    per-atom gather pattern (4 random LDG.64 z-pair corners + 2 LDG.256 elec/desolv bricks,
-    96 B) over maps of the workload's size; and plain random 8-B gathers from a 64 MiB
-    L2-resident buffer (context only: it understates what 32-B loads get from L2)."""
+    """Live hardware ceilings (tools/peaks.cu), best of 3 each:
+    * fp32_ffma2_tflops: packed FFMA2 throughput (8 independent chains per thread);
+    * l2_stream_gbs: coalesced L1-bypassing reads of a 32 MiB L2-resident buffer by every
+      SM -- the L2 read bandwidth ceiling;
+    * l2_sector_gbs: random whole 32-B sector reads of the same buffer -- the L2 ceiling
+      for scattered sectors, the access grain of the trilinear gathers;
+    * atom_pattern_gbs (context only): the score kernel's own 96-B atom pattern."""
     import ctypes
 
     path = ROOT / "tools" / "libvdpeaks.so"
     if not path.exists():
         return None
     lib = ctypes.CDLL(str(path))
-    lib.vdp_fp32_peak_tflops.restype = ctypes.c_double
-    lib.vdp_l2_gather_gbs.restype = ctypes.c_double
-    lib.vdp_l2_gather_gbs.argtypes = [ctypes.c_int64]
-    fp32 = max(lib.vdp_fp32_peak_tflops() for _ in range(3))
-    l2 = max(lib.vdp_l2_gather_gbs(64 << 20) for _ in range(3))
-    out = {"fp32_tflops": fp32, "l2_gather_8b_gbs": l2, "l2_gather_gbs": l2,
-           "l2_gather_src": "random 8-B gathers from a 64 MiB L2-resident buffer"}
-    if hasattr(lib, "vdp_atom_gather_gbs"):
-        lib.vdp_atom_gather_gbs.restype = ctypes.c_double
-        lib.vdp_atom_gather_gbs.argtypes = [ctypes.c_int, ctypes.c_int]
-        out["l2_gather_gbs"] = max(lib.vdp_atom_gather_gbs(grid_n, n_types) for _ in range(3))
-        out["l2_gather_src"] = (f"the kernel's own atom gather (4 random LDG.64 z-pairs of {n_types} "
-                                f"type maps + 2 LDG.256 brick pairs = 96 B) over {grid_n}^3 maps")
-    return out
+    for f in ("vdp_fp32_peak_tflops", "vdp_l2_stream_gbs", "vdp_l2_sector_gbs",
+              "vdp_atom_gather_gbs"):
+        getattr(lib, f).restype = ctypes.c_double
+    lib.vdp_l2_stream_gbs.argtypes = [ctypes.c_int64]
+    lib.vdp_l2_sector_gbs.argtypes = [ctypes.c_int64]
+    lib.vdp_atom_gather_gbs.argtypes = [ctypes.c_int, ctypes.c_int]
+    return {"fp32_ffma2_tflops": max(lib.vdp_fp32_peak_tflops() for _ in range(3)),
+            "l2_stream_gbs": max(lib.vdp_l2_stream_gbs(32 << 20) for _ in range(3)),
+            "l2_sector_gbs": max(lib.vdp_l2_sector_gbs(32 << 20) for _ in range(3)),
+            "atom_pattern_gbs": max(lib.vdp_atom_gather_gbs(grid_n, n_types) for _ in range(3))}
 
 
-def roofline_block(achieved_tf, fp32_peak, fp32_src, gather_bps, peaks, fpp, ctx,
-                   inbox_frac=None):
-    """Both rooflines of SURVEY 8(d); the binding one (lower poses/s ceiling) is primary.
-    Ridge = FP32 peak / L2 gather BW; the reference model's AI = fpp / (96 B * N)."""
-    bpp = 96 * int(ctx.n_atoms)
-    fp32 = {"achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-            "frac": achieved_tf / fp32_peak, "peak_source": fp32_src,
-            "algorithmic_flops_per_pose": fpp,
-            "ceiling_poses_per_s": fp32_peak * 1e12 / fpp}
-    out = {"bound": "fp32", "achieved": achieved_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-           "frac": achieved_tf / fp32_peak, "traffic": TRAFFIC_BYTES,
-           "traffic_source": TRAFFIC_SRC, "kernel": "vd::score_kernel<false,64,4,1> (packed-grid instantiation)",
-           "fp32": fp32, "arithmetic_intensity_flop_per_byte": fpp / bpp}
+def roofline_block(t_launch, n_poses, fpp, ctx, inbox_frac, peaks, traffic=None,
+                   traffic_src=None, kernel="vd::score_kernel<false,64,4,1>"):
+    """SURVEY 8(d) rooflines of one kernel launch from hardware ceilings.
+
+    Algorithmic work per pose is the reference's model (vd/bench.py:139-171):
+    32 flops per pair + 107 per atom, and 96 gather bytes per atom -- counted here
+    only for the in-box atoms, the only ones whose corners are loaded.  Ceilings:
+    FP32 = the spec 2 x 128 lanes x 148 SMs x 1.965 GHz (the live FFMA2 probe beside
+    it); L2 = the live coalesced L2-read probe (random-sector probe beside it); HBM =
+    MEASURED_PEAKS.json.  The binding roof is the one with the lower poses/s ceiling."""
+    n_atoms = int(ctx.n_atoms)
+    per_s = n_poses / t_launch
+    fp32_tf = fpp * per_s / 1e12
+    fp32 = {"achieved": fp32_tf, "peak": FP32_SPEC_TFLOPS, "unit": "TFLOP/s",
+            "frac": fp32_tf / FP32_SPEC_TFLOPS,
+            "peak_source": "spec: 2 x 128 FP32 lanes x 148 SMs x 1.965 GHz",
+            "flops_per_pose": fpp, "ceiling_poses_per_s": FP32_SPEC_TFLOPS * 1e12 / fpp}
+    inbox_b = 96.0 * n_atoms * inbox_frac
+    gather_gbs = inbox_b * per_s / 1e9
+    gather = {"achieved": gather_gbs, "unit": "GB/s", "bytes_per_pose_inbox": inbox_b,
+              "inbox_atom_fraction": inbox_frac,
+              "model_bytes_per_pose_all_atoms": 96 * n_atoms,
+              "achieved_model_all_atoms": 96.0 * n_atoms * per_s / 1e9}
+    hbm_peak = measured_peaks_file().get("hbm_gbs")
+    out = {"bound": "fp32", "achieved": fp32_tf, "peak": FP32_SPEC_TFLOPS, "unit": "TFLOP/s",
+           "frac": fp32_tf / FP32_SPEC_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+           "kernel": kernel, "ms_per_launch": 1e3 * t_launch, "poses_per_launch": n_poses,
+           "fp32": fp32, "l2_gather": gather}
     if peaks:
-        l2 = peaks["l2_gather_gbs"]
-        gather = {"achieved": gather_bps / 1e9, "peak": l2, "unit": "GB/s",
-                  "frac": gather_bps / 1e9 / l2, "bytes_per_pose": bpp,
-                  "peak_source": "measured live: " + peaks["l2_gather_src"]
-                                 + " (tools/peaks.cu), best of 3",
-                  "peak_8b_random_gbs": peaks["l2_gather_8b_gbs"],
-                  "inbox_atom_fraction": inbox_frac,
-                  "achieved_inbox_only": (gather_bps * inbox_frac / 1e9
-                                          if inbox_frac is not None else None),
-                  "frac_inbox_only": (gather_bps * inbox_frac / 1e9 / l2
-                                      if inbox_frac is not None else None),
-                  "note": "achieved counts 96 B for every atom (the reference's model, "
-                          "vd/bench.py:166-171); out-of-box atoms issue no gathers, so the "
-                          "bytes actually gathered are the in-box-only figure",
-                  "ceiling_poses_per_s": l2 * 1e9 / bpp}
-        out["l2_gather"] = gather
-        out["ridge_flop_per_byte"] = fp32_peak * 1e3 / l2
+        fp32["measured_ffma2_tflops"] = peaks["fp32_ffma2_tflops"]
+        fp32["frac_of_measured_ffma2"] = fp32_tf / peaks["fp32_ffma2_tflops"]
+        l2 = peaks["l2_stream_gbs"]
+        gather.update(peak=l2, frac=gather_gbs / l2,
+                      peak_source="measured live: coalesced L1-bypassing LDG.128 reads of a 32 MiB "
+                                  "L2-resident buffer by every SM (tools/peaks.cu), best of 3",
+                      l2_sector_peak_gbs=peaks["l2_sector_gbs"],
+                      frac_of_sector_peak=gather_gbs / peaks["l2_sector_gbs"],
+                      atom_pattern_gbs_context=peaks["atom_pattern_gbs"],
+                      ceiling_poses_per_s=l2 * 1e9 / inbox_b)
+        out["arithmetic_intensity_flop_per_byte"] = fpp / inbox_b
+        out["ridge_flop_per_byte"] = FP32_SPEC_TFLOPS * 1e3 / l2
         if gather["ceiling_poses_per_s"] < fp32["ceiling_poses_per_s"]:
-            out.update(bound="l2-gather", achieved=gather["achieved"], peak=l2, unit="GB/s",
-                       frac=gather["frac"])
+            out.update(bound="l2-gather", achieved=gather_gbs, peak=l2, unit="GB/s",
+                       frac=gather_gbs / l2)
+    if traffic and hbm_peak:
+        out["hbm"] = {"achieved": traffic / t_launch / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                      "frac": traffic / t_launch / 1e9 / hbm_peak,
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
     return out
 
 
@@ -307,12 +328,7 @@ def run_ours(args):
     parity_ok = bool(np.all((d <= 1e-3) | (d <= 1e-4 * np.abs(wt))))
 
     fpp = flops_per_pose(ctx)
-    achieved = fpp * N_POSES / (t_loc / args.steps) / 1e12
     peaks = measure_peaks(int(spec.dims[0]), len(gset.maps) - 2)
-    peak = peaks["fp32_tflops"] if peaks else FP32_SPEC_TFLOPS
-    peak_src = ("measured live on this GPU: packed-FFMA2 microbenchmark (tools/peaks.cu), "
-                "best of 3" if peaks else "spec-derived 2*128 lanes*148 SMs*1.965 GHz")
-    gather_bps = 96 * ctx.n_atoms * N_POSES / (t_loc / args.steps)
     # share of atoms inside the grid box (the kernel gathers only for those; the reference's
     # model counts every atom), from the device pose path on a sample of the genes
     smp = b.pose_population(genes_h[:8192], ctx)
@@ -335,8 +351,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": int(genes_h.nbytes),
                 "d2h_bytes_per_step": int(N_POSES * (8 + 8 + 4)),
                 "path": "CudaBackend.score_population_arrays (pinned numpy in/out)"},
-        "roofline": roofline_block(achieved, peak, peak_src, gather_bps, peaks, fpp, ctx,
-                                   inbox_frac),
+        "roofline": roofline_block(t_loc / args.steps, N_POSES, fpp, ctx, inbox_frac, peaks,
+                                   TRAFFIC_BYTES, TRAFFIC_SRC),
         "gpu_launches": int(launches),
         "parity_sample_ok": parity_ok,
         "clocks": clk.summary(),
@@ -370,7 +386,7 @@ def screening_leg(args, rank, world, dist, dev):
     generations), ligands split by index over ranks, records all-gathered over NCCL."""
     import torch
 
-    from paper_2509_12232_b200 import gridmaps, hostprep, synth
+    from paper_2509_12232_b200 import _abi, gridmaps, hostprep, synth
     from paper_2509_12232_b200.backend import CudaBackend
     from paper_2509_12232_b200.ga import GaConfig, _run
     from paper_2509_12232_b200.screening import gather_records, pack_records, shard_range
@@ -412,9 +428,43 @@ def screening_leg(args, rank, world, dist, dev):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_max = float(tt.item())
     evals = n * ga.population_size * (ga.generations + 1)
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = cpu_screen_baseline(gset, batch, ga, lo, args.cpu_seconds)
+    # cuda-exact (the reference-equal numerics) on the same shard: its throughput prices
+    # bit-exactness; its results are compared bit for bit with the oracle GA below
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0.record()
+    xbt, xbe, xba, xbg, _, _ = _run(grid, lset, 0, count, ga, 0, lo, _abi.MODE_EXACT, gmax,
+                                    trace=False)
+    ev1.record()
+    torch.cuda.synchronize(dev)
+    t_exact = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        tt = torch.tensor([t_exact], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_exact = float(tt.item())
+    cpu, par = None, None
+    if rank == 0:
+        from oracle import oracle, parity
+
+        stack = np.stack([gset.maps[l] for l in grid.labels]).astype(np.float32)
+        ligs = oracle.ligands_from_arrays(arrays, stack, spec)
+        par = {"tolerance": "|d| <= 1e-3 kcal/mol or |d|/|E| <= 1e-4 (north star)",
+               "fast_best_rescored": parity.rescore_summary(ligs, bt, be, ba, bg),
+               "exact_best_rescored": parity.rescore_summary(ligs, xbt, xbe, xba, xbg)}
+        if not args.no_cpu:
+            cpu, (k, og, obt) = cpu_screen_baseline(ligs, ga, spec, lo, args.cpu_seconds)
+            params = oracle.ga_params(ga, spec.origin, spec.upper)
+            ag = parity.ga_agreement(ligs[:k], params, 0, lo, bt[:k], bg[:k],
+                                     oracle_out=(og, obt))
+            rms = ag.pop("_rmsd")
+            ag.pop("_oracle_best_total")
+            ag["rmsd_of_disagreeing"] = [round(float(x), 3) for x in rms[~np.isnan(rms)]
+                                         if x > 0.5]
+            par["fast_vs_oracle_ga"] = ag
+            par["exact_vs_oracle_ga"] = {
+                "ligands": k, "bit_identical_best_total": int(np.sum(xbt[:k] == obt)),
+                "bit_identical_best_genes": int(np.sum(np.all(xbg[:k, :og.shape[1]] == og, axis=1)))}
     from paper_2509_12232_b200 import benchrecords as br
 
     npairs = float(arrays["pair_start"][-1]) / max(1, count)
@@ -423,11 +473,17 @@ def screening_leg(args, rank, world, dist, dev):
     return {"metric": "ligands docked/sec", "value": n / t_max, "unit": "ligands/s",
             "pose_evals_per_s": evals / t_max, "ligands": n, "ms": 1e3 * t_max,
             "ga": "pop 256 x 200 generations (cfg2 distribution, 64^3 grid, 3000-atom receptor)",
+            "mode": "fast",
             "workload": ("cfg2-screen-10k" if n == 10000 else "cfg3-screen-100k" if n == 100000
                          else f"cfg2-distribution x{n}"),
             "gathered_records": int(rec.shape[0]), "gather_ms": round(1e3 * t_gather, 3),
             "host_prep_s_per_rank": round(prep_s, 3),
             "timing": "CUDA events around vd_dock_batch (one persistent GA launch per atom-count bucket, buckets concurrent), max over ranks",
+            "exact_mode": {"value": n / t_exact, "unit": "ligands/s", "ms": 1e3 * t_exact,
+                           "note": "the same batch with reference-exact scoring (fp64 sums in "
+                                   "the reference's lane-8 order, libm-equal exp): bit-identical "
+                                   "to the oracle GA"},
+            **({"parity": par} if par else {}),
             **({"cpu_baseline": cpu} if cpu else {}),
             "_modeled": modeled}
 
@@ -464,7 +520,7 @@ def stress_leg(args, rank, world, dist, dev):
     torch.cuda.synchronize(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
-    _run(grid, lset, 0, hi - lo, ga, 0, lo, b._mode(), gmax, trace=False)
+    res = _run(grid, lset, 0, hi - lo, ga, 0, lo, b._mode(), gmax, trace=False)
     ev1.record()
     torch.cuda.synchronize(dev)
     t = ev0.elapsed_time(ev1) / 1e3
@@ -472,8 +528,30 @@ def stress_leg(args, rank, world, dist, dev):
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
+    # parity (outside the timed region): every rank-0 best re-scored by the oracle; the
+    # oracle GA (also the CPU baseline) on the first ligands, compared with the device's
+    bt, be, ba, bg, _, _ = res
+    par, cpu = None, None
+    if rank == 0:
+        from oracle import oracle, parity
+
+        stack = np.stack([gset.maps[l] for l in grid.labels]).astype(np.float32)
+        ligs = oracle.ligands_from_arrays(arrays, stack, spec)
+        par = {"tolerance": "|d| <= 1e-3 kcal/mol or |d|/|E| <= 1e-4 (north star)",
+               "fast_best_rescored": parity.rescore_summary(ligs, bt, be, ba, bg)}
+        if not args.no_cpu:
+            cpu, (k, og, obt) = cpu_screen_baseline(ligs, ga, spec, lo, args.cpu_seconds,
+                                                    label="cfg4")
+            ag = parity.ga_agreement(ligs[:k], oracle.ga_params(ga, spec.origin, spec.upper), 0,
+                                     lo, bt[:k], bg[:k], oracle_out=(og, obt))
+            rms = ag.pop("_rmsd")
+            ag.pop("_oracle_best_total")
+            ag["rmsd_of_disagreeing"] = [round(float(x), 3) for x in rms[~np.isnan(rms)]
+                                         if x > 0.5]
+            par["fast_vs_oracle_ga"] = ag
     npairs = float(arrays["pair_start"][-1]) / max(1, hi - lo)
     return {"metric": "ligands docked/sec", "value": n / t, "unit": "ligands/s",
+            **({"parity": par} if par else {}), **({"cpu_baseline": cpu} if cpu else {}),
             "pose_evals_per_s": n * 512 * 301 / t, "ligands": n, "ms": 1e3 * t,
             "workload": "cfg4-stress" if n == 2000 else f"cfg4-distribution x{n}",
             "ligand": f"{int(batch.n_atoms.max())} atoms, {int(batch.n_torsions.max())} torsions, "
@@ -513,58 +591,74 @@ def single_dock_leg(args, dev):
            "workload": "cfg0-single-dock", "best_total": float(r.best_score.total),
            "timing": "wall clock around ga.dock (host context prep + one GA launch + copies), "
                      "mean of the 7 fastest of 10"}
+    from oracle import parity
+
+    lig = oracle.Ligand(prepare_context(topo, gset))
+    params = oracle.ga_params(cfg, spec.origin, spec.upper)
+    og, obt, *_ = oracle.dock(lig, params, 0, 0)
+    rx = dock(topo, gset, cfg, backend=CudaBackend(mode="exact", device=dev.index))
+    out["parity"] = {
+        "oracle_best_total": float(obt),
+        "fast_within_tol": bool(parity.within_tol([r.best_score.total], [obt])[0]),
+        "fast_best_pose_rmsd": parity.rmsd(lig, r.best_genotype, og),
+        "exact_bit_identical": bool(np.float32(rx.best_score.total) == obt
+                                    and np.array_equal(rx.best_genotype, og)),
+        "tolerance": "|d| <= 1e-3 kcal/mol or |d|/|E| <= 1e-4, else RMSD <= 0.5 A"}
     if not args.no_cpu:
-        lig = oracle.Ligand(prepare_context(topo, gset))
-        params = oracle.ga_params(cfg, spec.origin, spec.upper)
         cs = []
         for _ in range(10):
             t0 = time.perf_counter()
             oracle.dock(lig, params, 0, 0)
             cs.append(time.perf_counter() - t0)
         out["cpu_baseline"] = {"value": float(np.mean(sorted(cs)[:7])), "unit": "s", "cores": 1,
-                               "kind": "port", "sample": "the same dock (restated GA, "
+                               "kind": "port", "cpu_model": cpu_model(), "sample": "the same dock (restated GA, "
                                "oracle/vd_ga_oracle.c) on one host core, 7 fastest of 10"}
     return out
 
 
-def cpu_screen_baseline(gset, batch, ga, index_base, seconds=10.0):
-    """The reference GA + scoring on the host (oracle/vd_ga_oracle.c: the restated GA, the
-    same per-ligand keys as the device, OpenMP over ligands) on the first ligands of the
-    screening batch, bounded to ~`seconds`: ligands docked/s on all host threads."""
+def cpu_screen_baseline(ligs, ga, spec, index_base, seconds=10.0, label="cfg2"):
+    """The reference GA + scoring on the host (oracle/vd_ga_oracle.c: the restated GA with
+    the device's per-ligand keys, oracle/vd_oracle.c scoring, OpenMP over ligands) on the
+    first ligands of the batch, bounded to ~`seconds`: ligands docked/s on all host
+    threads.  Also returns (k, best genes, best totals) of every ligand it docked (0..k-1),
+    for the GA parity comparison."""
     from oracle import oracle
-    from paper_2509_12232_b200 import chem
-    from paper_2509_12232_b200.context import prepare_context
 
-    labels = list(gset.maps)
-    gidx = {l: k for k, l in enumerate(labels)}
-    stack = np.stack([gset.maps[l] for l in labels]).astype(np.float32)
     cores = oracle.cores()
-    params = oracle.ga_params(ga, gset.spec.origin, gset.spec.upper)
-
-    def ligs(a, b):
-        out = []
-        for l in range(a, b):
-            ctx = prepare_context(batch.topology(l), gset)
-            amap = np.array([gidx[ctx.map_labels[k]] for k in ctx.atom_slot], np.int32)
-            out.append(oracle.Ligand(ctx, stack, amap, gidx[chem.ELEC_LABEL],
-                                     gidx[chem.DESOLV_LABEL]))
-        return out
-
-    k = min(len(batch), cores)  # probe: one ligand per thread
+    params = oracle.ga_params(ga, spec.origin, spec.upper)
+    k = min(len(ligs), cores)  # probe: one ligand per thread
     t0 = time.perf_counter()
-    oracle.dock_many(ligs(0, k), params, 0, index_base, n_threads=cores)
-    rate = k / max(time.perf_counter() - t0, 1e-9)
-    m = int(min(len(batch) - k, max(cores, rate * seconds)))
-    if m <= 0:
-        m, k = k, 0
-    sample = ligs(k, k + m)
-    t0 = time.perf_counter()
-    oracle.dock_many(sample, params, 0, index_base + k, n_threads=cores)
-    dt = time.perf_counter() - t0
-    return {"value": m / dt, "unit": "ligands/s", "cores": cores, "kind": "port",
-            "sample": f"ligands {k}..{k + m - 1} of the cfg2 batch, pop {ga.population_size} x "
-                      f"{ga.generations} generations, {dt:.1f} s on {cores} threads "
-                      "(oracle/vd_ga_oracle.c restated GA + oracle/vd_oracle.c scoring)"}
+    g0, b0, *_ = oracle.dock_many(ligs[:k], params, 0, index_base, n_threads=cores)
+    t_probe = time.perf_counter() - t0
+    rate = k / max(t_probe, 1e-9)
+    m = int(min(len(ligs) - k, max(cores, rate * seconds)))
+    if m <= 0 or rate * seconds < 2 * k:  # the probe already took the budget: report it
+        value, first, n_s, dt, genes, bests = rate, 0, k, t_probe, g0, b0
+    else:
+        t0 = time.perf_counter()
+        g1, b1, *_ = oracle.dock_many(ligs[k:k + m], params, 0, index_base + k, n_threads=cores)
+        dt = time.perf_counter() - t0
+        value, first, n_s = m / dt, k, m
+        w = max(g0.shape[1], g1.shape[1])
+        genes = np.zeros((k + m, w))
+        genes[:k, :g0.shape[1]], genes[k:, :g1.shape[1]] = g0, g1
+        bests = np.concatenate([b0, b1])
+    cpu = {"value": value, "unit": "ligands/s", "cores": cores, "kind": "port",
+           "cpu_model": cpu_model(),
+           "sample": f"ligands {first}..{first + n_s - 1} of the {label} batch, pop "
+                     f"{ga.population_size} x {ga.generations} generations, {dt:.1f} s on {cores} "
+                     "threads (oracle/vd_ga_oracle.c restated GA + oracle/vd_oracle.c scoring)"}
+    return cpu, (len(bests), genes, bests)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def cpu_baseline(ctx, genes, seconds=10.0):
@@ -585,6 +679,7 @@ def cpu_baseline(ctx, genes, seconds=10.0):
         oracle.dock_population(lig, genes[:n], n_threads=cores)
     dt = time.perf_counter() - t0
     return {"value": reps * n / dt, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{reps} pass(es) over the first {n} of the {N_POSES} cfg1 genotypes, "
                       f"{dt:.1f} s on {cores} threads (oracle/vd_oracle.c, bit-exact restatement "
                       "of SimdBackend.dock_population)"}
@@ -619,6 +714,7 @@ def run_reference(args):
         "config": {"workload": WORKLOAD, "poses_per_step": per_step, "grid_build_s": round(grid_s, 2),
                    "grid_built_on": grid_src},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{per_step} cfg1 genotypes per step (of the 1M workload); "
                                    "oracle/vd_oracle.c is bit-exact with the reference's simd "
                                    "backend (tests/test_oracle_golden.py)"},
@@ -627,7 +723,7 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def main():
+def main():  # noqa: C901
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -637,19 +733,62 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=16384)
     ap.add_argument("--csv", default=None, help="also write a BenchRecord CSV row (vd/bench.py schema)")
-    ap.add_argument("--screen-ligands", type=int, default=10000,
-                    help="cfg2 ligands for the ligands/s leg (0 disables)")
+    ap.add_argument("--screen-ligands", type=int, default=None,
+                    help="ligands for the screening leg (0 disables; default: cfg2's 10,000 at "
+                         "--gpus 1, cfg3's 100,000 sharded at --gpus > 1)")
     ap.add_argument("--stress-ligands", type=int, default=2000,
                     help="cfg4 ligands for the stress leg")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the cfg4 stress and cfg0 single-dock legs")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="CPU test of the rank launcher: gloo ranks, no GPU work")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.screen_ligands is None:  # BASELINE cfg2 (10k) on one GPU, cfg3 (100k) sharded
+        args.screen_ligands = 10000 if args.gpus == 1 else 100000
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args.gpus)  # does not return
+    world = env_int("WORLD_SIZE", 1)
+    if world != args.gpus:
+        sys.exit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.launch_check:
+        launch_check(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
+
+
+def relaunch(n: int):
+    """`python bench.py --gpus N` without torchrun: start N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1, exactly as the driver launches them."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
+def launch_check(args):
+    """The launcher's contract without a GPU: every rank joins one gloo group of
+    --gpus ranks, agrees on the max of a per-rank time, rank 0 prints one JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "launch_check": True, "n_gpus": world,
+                          "max_over_ranks": float(t.item()),
+                          "screen_ligands": args.screen_ligands}), flush=True)
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

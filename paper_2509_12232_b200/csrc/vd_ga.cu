@@ -565,9 +565,11 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             if (npp * L.tpp < 32) continue;  /* block_argmin's shuffles need whole warps */
             int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes, gv.yz != nullptr) * npp * L.tpp / 32;
             lay.r3 = 0;
-            if (!exact && npp == 32 && L.tpp == 4 && gv.yz != nullptr && !getenv("VD_GA_NO_R3")) {
-                /* small ligands: a third CTA fits in shared memory but not in 245 registers
-                   (<= 32 atoms: +5-6% ligands/s measured with the 168-register budget) */
+            if (!exact && npp == 32 && L.tpp == 4 && gv.yz != nullptr && nmax <= 32 &&
+                !getenv("VD_GA_NO_R3")) {
+                /* small ligands: a third CTA fits in shared memory but not in 245 registers.
+                   Measured with the 168-register budget (76 B of spills): <= 24 atoms +7%,
+                   25-32 atoms +8% ligands/s; only those buckets take it */
                 const int w3 = vd::ga_occupancy_r3(lay.base.bytes) * 4;
                 if (w3 > warps) {
                     warps = w3;

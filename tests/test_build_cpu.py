@@ -44,3 +44,11 @@ def test_score_kernel_fits_two_ctas_without_spills(kernel):
 def test_ga_kernel_has_no_spills(kernel):
     regs, spill = _resources(kernel)
     assert spill == 0, f"{kernel}: {spill} bytes of spills at {regs} registers"
+
+
+def test_ga_r3_variant_spills_stay_bounded():
+    """The 3-CTA register-budget GA variant (LAY 3, 168 registers; chosen only for packed
+    buckets of <= 32 atoms, where it measured +7-8%) spills a little by design: bound it."""
+    regs, spill = _resources("_ZN2vd9ga_kernelILb0ELi32ELi4ELi3E")
+    assert regs <= 168, regs
+    assert spill <= 128, f"{spill} bytes of spill stores at {regs} registers"

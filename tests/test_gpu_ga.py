@@ -259,3 +259,31 @@ def test_fast_mode_ga_identical_on_every_grid_layout(cuda, layout, monkeypatch):
     got, ref = run(layout), run("plain" if layout != "plain" else "brick")
     assert np.array_equal(got.trace.view(np.uint32), ref.trace.view(np.uint32))
     assert np.array_equal(got.best_genotype, ref.best_genotype)
+
+
+def test_r3_register_budget_variant_is_bit_identical(cuda, monkeypatch):
+    """Small packed-grid buckets (<= 32 atoms) run the 3-CTA register-budget GA variant
+    (LAY 3); VD_GA_NO_R3=1 forces the full-budget kernel.  Same code, same results."""
+    from paper_2509_12232_b200 import gridmaps, hostprep, synth
+    from paper_2509_12232_b200.ga import GaConfig, _run
+
+    spec = synth.config_grid_spec(2)
+    gset = gridmaps.build_grid_maps(synth.config_protein(2), spec, synth.CONFIGS[2].probe_types)
+    grid = cuda["fast"]._grid_for_set(gset)
+    batch = hostprep.TopologyBatch.synth(2, 0, 96)
+    keep = np.flatnonzero(batch.n_atoms <= 32)[:24]
+    assert len(keep) >= 8
+    arrays = hostprep.prepare_batch(batch, grid.labels)
+    lset = hostprep.ligand_set(arrays)
+    ga = GaConfig(population_size=256, generations=20, translation_bounds=(spec.origin, spec.upper))
+    gmax = 7 + int(batch.n_torsions.max())
+    from paper_2509_12232_b200 import _abi
+
+    def run():
+        return _run(grid, lset, 0, 96, ga, 4, 0, _abi.MODE_FAST, gmax)
+
+    a = run()
+    monkeypatch.setenv("VD_GA_NO_R3", "1")
+    b = run()
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))

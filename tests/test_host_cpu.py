@@ -346,3 +346,27 @@ def test_bench_records_csv_byte_stable_and_parseable():
                                     "lane_utilization", "status"]
     back = br.parse_csv(a)
     assert br.emit_csv(back) == a
+
+
+# --- bench.py launcher (the driver's N-GPU contract) ------------------------------------
+def test_bench_self_launches_gpus_ranks_gloo():
+    """`python bench.py --gpus 2` without torchrun starts 2 ranks through
+    torch.distributed.run; every rank joins one group and rank 0 prints n_gpus == 2."""
+    import json
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                        "--launch-check"], capture_output=True, text=True, env=env, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["max_over_ranks"] == 2.0 and d["screen_ligands"] == 100000
+    bad = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--launch-check"], capture_output=True, text=True,
+                         env={**env, "WORLD_SIZE": "1"}, timeout=120)
+    assert bad.returncode != 0 and "WORLD_SIZE=1" in bad.stderr

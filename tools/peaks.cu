@@ -5,7 +5,11 @@
 //   vdp_atom_gather: the score kernel's own per-atom gather pattern -- 4 LDG.64
 //                    z-pair corners of a random type map + 2 LDG.256 elec/desolv
 //                    bricks (96 B per atom) at uniformly random cells of
-//                    same-size packed maps; the ceiling of the inter stage
+//                    same-size packed maps (context only: a pattern, not a ceiling)
+//   vdp_l2_stream:   coalesced LDG.128 reads (L1-bypassing) of an L2-resident
+//                    buffer by every SM: the hardware L2 read bandwidth ceiling
+//   vdp_l2_sector:   random whole-sector (32-B, one LDG.256) reads of an
+//                    L2-resident buffer: the L2 ceiling for scattered sectors
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -70,6 +74,41 @@ __global__ void atom_gather_kernel(const float2 *__restrict__ zp, const float4 *
             ld256(ed + 2 * (int64_t)idx, e0, d0);
             ld256(ed + 2 * (int64_t)(idx + nyz), e1, d1);
             acc += a.x + b.y + c.x + d.y + e0.x + d0.w + e1.y + d1.z;
+        }
+    }
+    if (acc == 12345.0f) out[0] = acc;
+}
+
+__global__ void stream_kernel(const float4 *__restrict__ buf, int64_t n4, int passes, float *out)
+{
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int p = 0; p < passes; ++p) {
+        int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        for (; i + 3 * stride < n4; i += 4 * stride) {
+            const float4 a = __ldcg(buf + i), b = __ldcg(buf + i + stride);
+            const float4 c = __ldcg(buf + i + 2 * stride), d = __ldcg(buf + i + 3 * stride);
+            acc.x += a.x + b.y; acc.y += c.z + d.w; acc.z += a.w + c.x; acc.w += b.z + d.y;
+        }
+        for (; i < n4; i += stride) acc.x += __ldcg(buf + i).x;
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 12345.0f) out[0] = acc.x;
+}
+
+__global__ void sector_kernel(const float4 *__restrict__ buf, uint32_t mask, int iters, float *out)
+{
+    uint32_t h = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + 777u;
+    float acc = 0.f;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            h ^= h << 13; h ^= h >> 17; h ^= h << 5;
+            float4 lo, hi;
+            asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y),
+                           "=f"(hi.z), "=f"(hi.w)
+                         : "l"(buf + 2 * (size_t)(h & mask)));
+            acc += lo.x + hi.w;
         }
     }
     if (acc == 12345.0f) out[0] = acc;
@@ -174,4 +213,59 @@ extern "C" double vdp_atom_gather_gbs(int n, int n_types)
     cudaFree(a.out);
     const double atoms = (double)a.blocks * a.threads * a.iters * 4;
     return atoms * 96.0 / (ms * 1e-3) / 1e9;
+}
+
+struct SArgs { const float4 *buf; int64_t n4; int passes, blocks, threads; float *out; };
+static void launch_stream(void *p)
+{
+    SArgs *a = (SArgs *)p;
+    stream_kernel<<<a->blocks, a->threads>>>(a->buf, a->n4, a->passes, a->out);
+}
+
+/* GB/s of coalesced L2-resident reads (bytes <= ~1/3 of L2 keeps it resident on both dies) */
+extern "C" double vdp_l2_stream_gbs(int64_t bytes)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    SArgs a;
+    a.n4 = bytes / 16;
+    cudaMalloc((void **)&a.buf, a.n4 * sizeof(float4));
+    cudaMemset((void *)a.buf, 0, a.n4 * sizeof(float4));
+    cudaMalloc(&a.out, sizeof(float));
+    a.blocks = sms * 4;
+    a.threads = 512;
+    a.passes = 16;
+    const float ms = time_it(launch_stream, &a);
+    cudaFree((void *)a.buf);
+    cudaFree(a.out);
+    return (double)a.n4 * 16.0 * a.passes / (ms * 1e-3) / 1e9;
+}
+
+struct QArgs { const float4 *buf; uint32_t mask; int iters, blocks, threads; float *out; };
+static void launch_sector(void *p)
+{
+    QArgs *a = (QArgs *)p;
+    sector_kernel<<<a->blocks, a->threads>>>(a->buf, a->mask, a->iters, a->out);
+}
+
+/* GB/s of random 32-B sector reads from an L2-resident buffer (bytes: power of two) */
+extern "C" double vdp_l2_sector_gbs(int64_t bytes)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    QArgs a;
+    const int64_t sectors = bytes / 32;
+    cudaMalloc((void **)&a.buf, sectors * 32);
+    cudaMemset((void *)a.buf, 0, sectors * 32);
+    cudaMalloc(&a.out, sizeof(float));
+    a.mask = (uint32_t)(sectors - 1);
+    a.blocks = sms * 8;
+    a.threads = 256;
+    a.iters = 128;
+    const float ms = time_it(launch_sector, &a);
+    cudaFree((void *)a.buf);
+    cudaFree(a.out);
+    return (double)a.blocks * a.threads * a.iters * 8 * 32.0 / (ms * 1e-3) / 1e9;
 }
