@@ -164,6 +164,10 @@ int vd_synth_fill(uint64_t seed, int64_t first, int count, int h_lo, int h_hi, d
 
 /* device-side counters of the last call on this thread (kernel launches) */
 int vd_last_launch_count(int64_t *launches);
+/* staging pipelines (3 streams + ring slots) ever created on `device`: host-buffer calls
+ * lease one from a process-wide pool, so this is the peak number of concurrent calls,
+ * not the number of threads that ever called */
+int vd_pipe_count(int device);
 
 /* ---- test probes (parity checks of the GA's device randomness) ------------
  * They run the GA kernel's own device functions on chosen inputs, so the

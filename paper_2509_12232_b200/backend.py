@@ -30,26 +30,91 @@ _MODES = {"fast": _abi.MODE_FAST, "exact": _abi.MODE_EXACT}
 
 
 class _DeviceCache:
-    """id(obj) -> value, dropped when obj is garbage collected."""
+    """id(obj) -> value, dropped when obj is garbage collected.  Single-flight: when
+    several threads ask for the same object at once (the reference's screen_batch workers
+    share one backend, vd/screening.py:212-222), one builds and the others wait for it."""
 
     def __init__(self):
         self._d = {}
+        self._inflight = {}
         self._lock = threading.Lock()
 
     def get(self, obj, make):
         key = id(obj)
-        with self._lock:
-            hit = self._d.get(key)
-            if hit is not None:
-                return hit
-        val = make()
-        with self._lock:
-            self._d[key] = val
+        while True:
+            with self._lock:
+                hit = self._d.get(key)
+                if hit is not None:
+                    return hit
+                ev = self._inflight.get(key)
+                owner = ev is None
+                if owner:
+                    ev = self._inflight[key] = threading.Event()
+            if owner:
+                break
+            ev.wait()  # the owner finished (or failed: then this thread retries as owner)
         try:
-            weakref.finalize(obj, self._d.pop, key, None)
-        except TypeError:  # not weak-referenceable: keep for process lifetime
-            pass
-        return val
+            val = make()
+            with self._lock:
+                self._d[key] = val
+            try:
+                weakref.finalize(obj, self._d.pop, key, None)
+            except TypeError:  # not weak-referenceable: keep for process lifetime
+                pass
+            return val
+        finally:
+            with self._lock:
+                self._inflight.pop(key, None)
+            ev.set()
+
+
+class _MapPool:
+    """Device grids for reference ScoringContexts, deduplicated by content.
+
+    A reference context carries a private copy of its maps (`map_stack`, the sorted
+    needed type maps then @elec/@desolv, vd/scoring/__init__.py:158-161), and the
+    reference's screen_batch keeps one context per ligand alive for the whole batch
+    (vd/screening.py:195-203).  Uploading each stack would cost ~10-50 MB of device memory
+    per ligand.  Instead every distinct map (same grid geometry, equal values) is uploaded
+    once into a shared grid; a context only maps its slots to indices of that grid.  When
+    a context brings a map not seen before, the pool's grid is rebuilt with it appended
+    (grids already handed out stay valid for the contexts that hold them)."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._pools = {}
+
+    @staticmethod
+    def _digest(m):
+        import hashlib
+
+        sample = np.ascontiguousarray(m[::3, ::3, ::3])
+        return hashlib.blake2b(sample.tobytes(), digest_size=16).digest()
+
+    def resolve(self, ctx):
+        """(DeviceGrid, slot -> grid map index) for a context's map stack."""
+        stack = np.asarray(ctx.map_stack, np.float32)
+        key = (stack.shape[1:], tuple(np.asarray(ctx.box_lo, np.float32).tolist()),
+               tuple(np.asarray(ctx.box_hi, np.float32).tolist()), float(np.float32(ctx.spacing)))
+        with self._lock:
+            st = self._pools.setdefault(key, {"maps": [], "by_digest": {}, "grid": None})
+            where = []
+            for k in range(stack.shape[0]):
+                m = stack[k]
+                cands = st["by_digest"].setdefault(self._digest(m), [])
+                idx = next((i for i in cands if np.array_equal(st["maps"][i], m)), None)
+                if idx is None:
+                    idx = len(st["maps"])
+                    st["maps"].append(np.array(m, np.float32, copy=True))
+                    cands.append(idx)
+                where.append(idx)
+            if st["grid"] is None or st["grid"].n_maps < len(st["maps"]):
+                st["grid"] = _abi.grid_from_stack(np.stack(st["maps"]), key[1], key[2], key[3])
+            return st["grid"], np.asarray(where, np.int32)
+
+    def n_device_maps(self) -> int:
+        with self._lock:
+            return sum(len(st["maps"]) for st in self._pools.values())
 
 
 class CudaBackend:
@@ -65,6 +130,7 @@ class CudaBackend:
         self.device = device
         self._grids = _DeviceCache()
         self._ligs = _DeviceCache()
+        self._pool = _MapPool()
         _abi.lib()  # raise BackendUnavailable now, not mid-run
 
     # -- device state ------------------------------------------------------
@@ -90,11 +156,10 @@ class CudaBackend:
                 slot_to_map = np.array([where[l] for l in ctx.map_labels], np.int32)
                 atom_map = slot_to_map[np.asarray(ctx.atom_slot, np.int64)]
                 elec, desolv = where[chem.ELEC_LABEL], where[chem.DESOLV_LABEL]
-            else:  # a reference ScoringContext: its private map stack is the grid
-                stack = ctx.map_stack
-                grid = _abi.grid_from_stack(stack, ctx.box_lo, ctx.box_hi, ctx.spacing)
-                atom_map = np.asarray(ctx.atom_slot, np.int32)
-                elec, desolv = stack.shape[0] - 2, stack.shape[0] - 1
+            else:  # a reference ScoringContext: its private map stack, deduplicated
+                grid, where = self._pool.resolve(ctx)
+                atom_map = where[np.asarray(ctx.atom_slot, np.int64)]
+                elec, desolv = int(where[-2]), int(where[-1])
             view = _PaddedContext(ctx, n)
             atom_map = _pad(atom_map, n, np.int32)
             return grid, _abi.LigandSet([view], [atom_map], elec, desolv)

@@ -203,25 +203,72 @@ struct Pipe {
     int64_t out_cap = 0;
 };
 
-static Pipe *pipe_for_device()
-{
-    static thread_local std::map<int, Pipe> pipes;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    auto it = pipes.find(dev);
-    if (it != pipes.end()) return &it->second;
-    Pipe p;
-    cudaStreamCreateWithFlags(&p.h, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&p.k, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&p.d, cudaStreamNonBlocking);
-    for (int r = 0; r < kRing; ++r) {
-        cudaEventCreateWithFlags(&p.eh[r], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&p.ek[r], cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&p.ed[r], cudaEventDisableTiming);
+/* Process-wide pool of pipes per device.  A call leases one for its duration, so
+ * concurrent callers never share staging slots, and threads that come and go (the
+ * reference's per-call worker pools) reuse pipes instead of leaking one each: the pool
+ * holds at most as many pipes as calls ever ran at once on that device.  A pipe handed
+ * back with copies still in flight is safe to reuse: its streams are in order and every
+ * slot reuse waits on the slot's last events. */
+class PipeLease {
+  public:
+    PipeLease()
+    {
+        cudaGetDevice(&dev_);
+        {
+            std::lock_guard<std::mutex> lk(mu());
+            auto &fl = free_list()[dev_];
+            if (!fl.empty()) {
+                p_ = fl.back();
+                fl.pop_back();
+                return;
+            }
+        }
+        p_ = new Pipe();
+        cudaStreamCreateWithFlags(&p_->h, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&p_->k, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&p_->d, cudaStreamNonBlocking);
+        for (int r = 0; r < kRing; ++r) {
+            cudaEventCreateWithFlags(&p_->eh[r], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&p_->ek[r], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&p_->ed[r], cudaEventDisableTiming);
+        }
+        cudaEventCreateWithFlags(&p_->start, cudaEventDisableTiming);
+        std::lock_guard<std::mutex> lk(mu());
+        ++created()[dev_];
     }
-    cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
-    return &(pipes[dev] = p);
-}
+    ~PipeLease()
+    {
+        std::lock_guard<std::mutex> lk(mu());
+        free_list()[dev_].push_back(p_);
+    }
+    PipeLease(const PipeLease &) = delete;
+    PipeLease &operator=(const PipeLease &) = delete;
+    Pipe *operator->() const { return p_; }
+    static int pipes_created(int dev)
+    {
+        std::lock_guard<std::mutex> lk(mu());
+        return created()[dev];
+    }
+
+  private:
+    static std::mutex &mu()
+    {
+        static std::mutex m;
+        return m;
+    }
+    static std::map<int, std::vector<Pipe *>> &free_list()
+    {
+        static auto *m = new std::map<int, std::vector<Pipe *>>();  /* never destroyed: no CUDA calls at exit */
+        return *m;
+    }
+    static std::map<int, int> &created()
+    {
+        static auto *m = new std::map<int, int>();
+        return *m;
+    }
+    int dev_ = 0;
+    Pipe *p_ = nullptr;
+};
 }  // namespace vdi
 
 vd::LigView vd_ligands::view(int l) const
@@ -260,6 +307,11 @@ int vd_last_launch_count(int64_t *launches)
 {
     *launches = vdi::g_launches;
     return 0;
+}
+
+int vd_pipe_count(int device)
+{
+    return vdi::PipeLease::pipes_created(device);
 }
 
 int vd_device_count(int *count)
@@ -511,7 +563,7 @@ static int score_common(const vd_grid *g, const vd_ligands *s, int lig, const vo
     /* chunked pipeline through a ring of device staging slots (see Pipe).  Chunks of CH
        poses, the last CH split in halves and quarters so the final kernel + copy-out that
        trail the last copy-in are short. */
-    vdi::Pipe *pp = vdi::pipe_for_device();
+    vdi::PipeLease pp;
     static const int64_t chunk_env = getenv("VD_CHUNK") ? atoll(getenv("VD_CHUNK")) : 0;
     const int64_t CH = std::min<int64_t>(P, chunk_env > 0 ? chunk_env : (1 << 17));
     std::vector<std::pair<int64_t, int64_t>> chunks;  /* (offset, count) */
