@@ -11,6 +11,7 @@
  * Each entry replaces one reference seam (paths under
  * /root/reference/pkg/src/vecdock):
  *
+ *   vd_grid_load_mugd                 grids.py:269-303 read_grid_set (MUGD file -> device)
  *   vd_grid_create / vd_grid_build    grids.py:83-119 GridMapSet, grids.py:122-202
  *                                     build_grid_maps; the map stack of
  *                                     scoring/__init__.py:158-161 becomes one
@@ -78,6 +79,21 @@ int vd_grid_n_maps(const vd_grid *g);
 enum vd_layout { VD_LAYOUT_PLAIN = 0, VD_LAYOUT_BRICK = 1, VD_LAYOUT_ZPAIR = 2 };
 int vd_grid_layout(const vd_grid *g);
 int vd_grid_download(const vd_grid *g, float *out /* (n_maps, nx, ny, nz) host */);
+
+/* MUGD grid files (vd/grids.py:232-303 write_grid_set / read_grid_set): payloads are
+ * read into pinned host staging, copied as stored (x fastest) and transposed on the
+ * device into the z-fastest stack; maps keep file order.  Format errors return -2 with
+ * the reference's GridFormatError message in vd_last_error(); other failures -1.
+ * vd_mugd_read_header fills `info` and, when `labels` is non-null, the map labels as
+ * consecutive NUL-terminated strings (info->labels_bytes in total). */
+typedef struct {
+    int32_t n_maps, nx, ny, nz;
+    float origin[3];
+    float spacing;
+    int32_t labels_bytes;
+} vd_mugd_info;
+int vd_mugd_read_header(const char *path, vd_mugd_info *info, char *labels, int labels_cap);
+int vd_grid_load_mugd(const char *path, vd_grid **out);
 int vd_grid_destroy(vd_grid *g);
 
 /* ---- ligand set (ScoringContext records, CSR over L ligands) ------------- */

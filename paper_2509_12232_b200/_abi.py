@@ -53,6 +53,11 @@ class VdWeights(C.Structure):
                 ("desolv", C.c_double)]
 
 
+class VdMugdInfo(C.Structure):
+    _fields_ = [("n_maps", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("origin", C.c_float * 3), ("spacing", C.c_float), ("labels_bytes", C.c_int32)]
+
+
 class VdGaParams(C.Structure):
     _fields_ = [("pop", C.c_int32), ("generations", C.c_int32), ("tournament", C.c_int32),
                 ("elitism", C.c_int32), ("cx_rate", C.c_double), ("mut_rate", C.c_double),
@@ -66,6 +71,7 @@ EXPORTS = (
     "vd_ligands_create", "vd_ligands_n_torsions", "vd_ligands_destroy", "vd_score_genes",
     "vd_score_poses", "vd_pose_genes", "vd_dock_batch", "vd_last_launch_count", "vd_pipe_count",
     "vd_prepare_count", "vd_prepare_fill", "vd_synth_count", "vd_synth_fill",
+    "vd_mugd_read_header", "vd_grid_load_mugd",
     "vd_debug_rng", "vd_debug_ga_init", "vd_debug_ga_breed", "vd_debug_pose_genes",
 )
 
@@ -86,6 +92,8 @@ def load_library(path: Path = LIB_PATH):
                                 i32, vp, C.c_double, vp]
     L.vd_grid_n_maps.argtypes = [vp]
     L.vd_grid_layout.argtypes = [vp]
+    L.vd_mugd_read_header.argtypes = [C.c_char_p, vp, vp, i32]
+    L.vd_grid_load_mugd.argtypes = [C.c_char_p, vp]
     L.vd_grid_download.argtypes = [vp, vp]
     L.vd_grid_destroy.argtypes = [vp]
     L.vd_ligands_create.argtypes = [vp, vp]
@@ -254,6 +262,52 @@ def build_grid_device(protein, spec, probe_types, weights, table, cutoff) -> Dev
     labels = list(probe_types) + ["@elec", "@desolv"]
     return DeviceGrid(h, len(probe) + 2, spec.dims, np.asarray(spec.origin, np.float32),
                       np.asarray(spec.upper, np.float32), np.float32(spec.spacing), labels)
+
+
+def _mugd_check(rc: int, what: str):
+    if rc == -2:
+        from .gridmaps import GridFormatError
+
+        raise GridFormatError(lib_err())
+    check(rc, what)
+
+
+def lib_err() -> str:
+    msg = host_lib().vd_last_error()
+    return msg.decode() if msg else ""
+
+
+def mugd_header(path) -> tuple:
+    """(VdMugdInfo, [labels]) of a MUGD file (host-only: no device needed)."""
+    L = host_lib()
+    info = VdMugdInfo()
+    p = os.fsencode(os.fspath(path))
+    rc = L.vd_mugd_read_header(p, C.byref(info), None, 0)
+    if rc == -2:
+        from .gridmaps import GridFormatError
+
+        raise GridFormatError(lib_err())
+    if rc:
+        raise OSError(lib_err())
+    buf = C.create_string_buffer(max(1, info.labels_bytes))
+    if L.vd_mugd_read_header(p, C.byref(info), buf, len(buf)):
+        raise OSError(lib_err())
+    labels = buf.raw[:info.labels_bytes].split(b"\0")[:-1] if info.labels_bytes else []
+    return info, [l.decode("utf-8") for l in labels]
+
+
+def grid_from_mugd(path, device=None) -> DeviceGrid:
+    """A MUGD file straight into a device grid (pinned staging + device transpose)."""
+    info, labels = mugd_header(path)
+    ensure_device(device)
+    h = C.c_void_p()
+    _mugd_check(lib().vd_grid_load_mugd(os.fsencode(os.fspath(path)), C.byref(h)),
+                "vd_grid_load_mugd")
+    dims = (info.nx, info.ny, info.nz)
+    origin = tuple(float(v) for v in info.origin)
+    upper = tuple(o + (d - 1) * float(info.spacing) for o, d in zip(origin, dims))
+    return DeviceGrid(h, info.n_maps, dims, np.asarray(origin, np.float32),
+                      np.asarray(upper, np.float32), np.float32(info.spacing), labels)
 
 
 def build_grid(protein, spec, probe_types, weights, table, cutoff, device=None) -> np.ndarray:

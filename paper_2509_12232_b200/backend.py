@@ -135,6 +135,10 @@ class CudaBackend:
 
     # -- device state ------------------------------------------------------
     def _grid_for_set(self, grid_set):
+        dg = getattr(grid_set, "device_grid", None)
+        if dg is not None:  # loaded straight onto the device (gridmaps.load_grid_set)
+            return dg
+
         def make():
             labels = list(grid_set.maps)
             stack = np.stack([grid_set.maps[l] for l in labels])

@@ -9,6 +9,7 @@ messages).  The map *builder* is the B200 kernel `vd_build_grid`
 * build_grid_maps ....... vd/grids.py:122-202 (device: csrc/gridbuild.cu)
 * trilinear_lookup ...... vd/grids.py:205-229
 * write/read_grid_set ... vd/grids.py:232-303 (MUGD; x-fastest payloads)
+* load_grid_set ......... read_grid_set straight to the device (csrc/vd_mugd.cu)
 """
 
 from __future__ import annotations
@@ -195,3 +196,83 @@ def read_grid_set(source) -> GridMapSet:
     finally:
         if own:
             source.close()
+
+
+class _DeviceMaps(dict):
+    """Label -> map view of a device-loaded set: the keys are known from the header,
+    the host values are downloaded once, on first access (the device path never needs
+    them; the oracle and the reference-style map_stack do)."""
+
+    def __init__(self, dgrid):
+        super().__init__()
+        self._dgrid = dgrid
+        self._labels = list(dgrid.labels)
+        self._host = None
+
+    def _fill(self):
+        if self._host is None:
+            stack = self._dgrid.download()
+            for k, l in enumerate(self._labels):
+                a = stack[k]
+                a.flags.writeable = False
+                dict.__setitem__(self, l, a)
+            self._host = True
+
+    def __contains__(self, label):
+        return label in self._labels
+
+    def __iter__(self):
+        return iter(self._labels)
+
+    def __len__(self):
+        return len(self._labels)
+
+    def keys(self):
+        return list(self._labels)
+
+    def __getitem__(self, label):
+        if label not in self._labels:
+            raise KeyError(label)
+        self._fill()
+        return dict.__getitem__(self, label)
+
+    def items(self):
+        self._fill()
+        return [(l, dict.__getitem__(self, l)) for l in self._labels]
+
+    def values(self):
+        return [v for _, v in self.items()]
+
+
+class DeviceGridMapSet:
+    """A GridMapSet whose maps were loaded onto the device from a MUGD file."""
+
+    def __init__(self, spec: GridSpec, dgrid):
+        self.spec = spec
+        self.device_grid = dgrid
+        self.maps = _DeviceMaps(dgrid)
+
+    @property
+    def elec_map(self):
+        return self.maps[ELEC_LABEL]
+
+    @property
+    def desolv_map(self):
+        return self.maps[DESOLV_LABEL]
+
+    @property
+    def type_labels(self):
+        return [k for k in self.maps if not k.startswith("@")]
+
+
+def load_grid_set(source, device: int | None = None) -> DeviceGridMapSet:
+    """read_grid_set (vd/grids.py:269-303) with the payloads going file -> pinned host
+    staging -> device, transposed there to the z-fastest layout (csrc/vd_mugd.cu).  Same
+    GridFormatError messages as read_grid_set."""
+    from . import _abi
+
+    dgrid = _abi.grid_from_mugd(source, device)
+    info, _ = _abi.mugd_header(source)
+    spec = GridSpec(tuple(float(v) for v in info.origin), float(info.spacing),
+                    (info.nx, info.ny, info.nz))
+    return DeviceGridMapSet(spec, dgrid)

@@ -260,7 +260,34 @@ def make_grids_small():
     np.savez_compressed(OUT / "grids_small.npz", **d)
 
 
+def make_mugd():
+    """MUGD streams written by the REFERENCE's write_grid_set (vd/grids.py:232-258), with
+    the maps they hold: the grids_small 'b' set (16^3 x 9 maps, built by the reference) and
+    a random non-cubic one (13 x 7 x 37, 3 maps) for the device transpose's edges."""
+    sys.path.insert(0, str(REF_TESTS))
+    from conftest import make_pocket_protein
+
+    b = make_pocket_protein(41, 50, radius=5.5, table=TABLE)
+    spec_b = rgrids.GridSpec.centered((0.0, 0.0, 0.0), (16, 16, 16), 0.55)
+    gb = rgrids.build_grid_maps(b, spec_b, TABLE.labels, table=TABLE)
+    rgrids.write_grid_set(gb, OUT / "ref_grid_b.mugd")
+    rng = np.random.default_rng(77)
+    spec_r = rgrids.GridSpec((-1.25, 0.5, 3.0), 0.375, (13, 7, 37))
+    maps_r = {l: rng.normal(0, 5, spec_r.dims).astype(np.float32) for l in ("C", "@elec", "@desolv")}
+    gr = rgrids.GridMapSet(spec=spec_r, maps=maps_r)
+    rgrids.write_grid_set(gr, OUT / "ref_grid_odd.mugd")
+    d = {}
+    for tag, g in (("b", gb), ("odd", gr)):
+        d[f"{tag}__labels"] = np.array(list(g.maps))
+        d[f"{tag}__stack"] = np.stack([g.maps[l] for l in g.maps]).astype(np.float32)
+        d[f"{tag}__origin"] = np.array(g.spec.origin)
+        d[f"{tag}__spacing"] = np.float64(g.spec.spacing)
+        d[f"{tag}__dims"] = np.array(g.spec.dims)
+    np.savez_compressed(OUT / "mugd_cases.npz", **d)
+
+
 if __name__ == "__main__":
+    make_mugd()
     make_golden_case()
     make_pop_cases()
     make_pairlists()

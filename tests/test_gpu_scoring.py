@@ -332,3 +332,96 @@ def test_concurrent_threads_different_ligands(cuda):
         for k, got in ex.map(work, range(24)):
             for x, y in zip(got, want[k]):
                 assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+def test_reference_contexts_share_deduplicated_device_maps():
+    """300 contexts that each carry a private copy of the same map stack (what the
+    reference's screen_batch keeps alive, vd/screening.py:195-203) upload the maps once:
+    device memory stays flat and every context scores exactly as with the shared grid."""
+    import dataclasses
+
+    import torch
+
+    from paper_2509_12232_b200 import hostprep, synth
+    from paper_2509_12232_b200.backend import CudaBackend
+    from paper_2509_12232_b200.context import prepare_context
+
+    c = fx.pop_case("cfg1")
+    gset = c["grid"]
+    b = CudaBackend(mode="fast", device=0)
+    batch = hostprep.TopologyBatch.synth(2, 0, 300)
+    ctxs = []
+    free0 = torch.cuda.mem_get_info(0)[0]
+    for l in range(len(batch)):
+        try:
+            ctx = prepare_context(batch.topology(l), gset, table=fx.TABLE)
+        except ValueError:
+            continue  # type without a map in the small fixture grid
+        own = np.array(ctx.map_stack, copy=True)  # a private copy per context
+        ref_like = dataclasses.replace(ctx, grid_set=None, explicit_stack=own)
+        genes = synth.random_genes(l, 64, ctx.n_torsions, gset.spec.origin, gset.spec.upper)
+        got = b.score_population_arrays(genes, ref_like)
+        want = b.score_population_arrays(genes, ctx)
+        for x, y in zip(got, want):
+            assert np.array_equal(x, y)
+        ctxs.append(ref_like)
+    assert len(ctxs) >= 100
+    used = free0 - torch.cuda.mem_get_info(0)[0]
+    assert b._pool.n_device_maps() <= len(gset.maps)
+    assert used < 256 << 20, f"{used / 2**20:.0f} MiB for {len(ctxs)} contexts"
+
+
+def test_short_lived_threads_reuse_staging_pipes(cuda):
+    """Worker threads that come and go (a fresh pool per screen_batch call) lease staging
+    pipelines from one process-wide pool: the count is bounded by the concurrency, not by
+    how many threads ever called."""
+    import threading
+
+    from paper_2509_12232_b200 import _abi
+
+    c = fx.pop_case("cfg0")
+    want = cuda["fast"].score_population_arrays(c["genes"], c["ctx"])
+    before = _abi.lib().vd_pipe_count(0)
+    for _ in range(10):
+        ts = []
+        errs = []
+
+        def work():
+            got = cuda["fast"].score_population_arrays(c["genes"], c["ctx"])
+            if not all(np.array_equal(x, y) for x, y in zip(got, want)):
+                errs.append("mismatch")
+
+        for _ in range(3):
+            ts.append(threading.Thread(target=work))
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        assert not errs
+    assert _abi.lib().vd_pipe_count(0) - before <= 3
+
+
+@pytest.mark.parametrize("tag", ["b", "odd"])
+def test_mugd_file_loads_straight_to_device(cuda, tag):
+    """A MUGD stream written by the reference's write_grid_set (vd/grids.py:232-258) goes
+    file -> pinned staging -> device transpose (csrc/vd_mugd.cu): the device stack equals
+    the reference's maps bit for bit, and scoring through the loaded set equals scoring
+    through the host-read set."""
+    from paper_2509_12232_b200 import gridmaps, synth
+    from paper_2509_12232_b200.context import prepare_context
+
+    d = fx.load("mugd_cases")
+    path = fx.GOLDEN / f"ref_grid_{tag}.mugd"
+    dset = gridmaps.load_grid_set(path)
+    stack = dset.device_grid.download()
+    assert np.array_equal(stack.view(np.uint32), d[f"{tag}__stack"].view(np.uint32))
+    assert list(dset.maps) == [str(l) for l in d[f"{tag}__labels"]]
+    hset = gridmaps.read_grid_set(path)
+    assert dset.spec == hset.spec
+    if tag == "b":
+        topo = synth.make_ligand(5, 18, 6, 4)
+        genes = synth.random_genes(9, 2048, topo.n_torsions, hset.spec.origin, hset.spec.upper)
+        a = cuda["exact"].score_population_arrays(genes, prepare_context(topo, dset, table=fx.TABLE))
+        b = cuda["exact"].score_population_arrays(genes, prepare_context(topo, hset, table=fx.TABLE))
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
