@@ -184,6 +184,12 @@ int vd_last_launch_count(int64_t *launches);
  * lease one from a process-wide pool, so this is the peak number of concurrent calls,
  * not the number of threads that ever called */
 int vd_pipe_count(int device);
+/* checked build (libvdb200_checked.so, -DVD_CHECKED): OR of the device bounds/invariant
+ * flags raised since the last clear (bit = site, csrc/vd_device.cuh VD_SITE_*); returns 1.
+ * clear < 0 first runs a self-test that raises VD_SITE_TILE and VD_SITE_POP (bits 6, 5)
+ * from the score and GA translation units, then reads and clears.
+ * The production build returns 0 and *flags = 0. */
+int vd_debug_check_flags(uint32_t *flags, int clear);
 
 /* ---- test probes (parity checks of the GA's device randomness) ------------
  * They run the GA kernel's own device functions on chosen inputs, so the

@@ -69,7 +69,7 @@ EXPORTS = (
     "vd_abi_version", "vd_last_error", "vd_device_count", "vd_init", "vd_grid_create",
     "vd_grid_build", "vd_grid_n_maps", "vd_grid_layout", "vd_grid_download", "vd_grid_destroy",
     "vd_ligands_create", "vd_ligands_n_torsions", "vd_ligands_destroy", "vd_score_genes",
-    "vd_score_poses", "vd_pose_genes", "vd_dock_batch", "vd_last_launch_count", "vd_pipe_count",
+    "vd_score_poses", "vd_pose_genes", "vd_dock_batch", "vd_last_launch_count", "vd_pipe_count", "vd_debug_check_flags",
     "vd_prepare_count", "vd_prepare_fill", "vd_synth_count", "vd_synth_fill",
     "vd_mugd_read_header", "vd_grid_load_mugd",
     "vd_debug_rng", "vd_debug_ga_init", "vd_debug_ga_breed", "vd_debug_pose_genes",
@@ -106,6 +106,7 @@ def load_library(path: Path = LIB_PATH):
                                 vp, vp]
     L.vd_last_launch_count.argtypes = [vp]
     L.vd_pipe_count.argtypes = [i32]
+    L.vd_debug_check_flags.argtypes = [vp, i32]
     L.vd_prepare_count.argtypes = [i32] + [vp] * 8
     L.vd_prepare_fill.argtypes = [i32] + [vp] * 8 + [vp, i32, vp, vp, C.c_double] + [vp] * 16
     L.vd_synth_count.argtypes = [u64, i64, i32, i32, i32, C.c_double, i32, i32, vp, vp]

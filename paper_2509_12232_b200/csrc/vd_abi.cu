@@ -174,6 +174,7 @@ vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map)
     v.ed = ed_for(g, elec_map, desolv_map);
     v.yz = v.ed ? g->d_yz : nullptr;
     v.maps = g->d_maps;
+    v.n_maps = g->n_maps;
     v.nx = g->nx;
     v.ny = g->ny;
     v.nz = g->nz;
@@ -312,6 +313,23 @@ int vd_last_launch_count(int64_t *launches)
 int vd_pipe_count(int device)
 {
     return vdi::PipeLease::pipes_created(device);
+}
+
+int vd_debug_check_flags(uint32_t *flags, int clear)
+{
+#ifdef VD_CHECKED
+    if (clear < 0) {  /* self-test: each translation unit raises one known flag */
+        vdi::chk_selftest_score();
+        vdi::chk_selftest_ga();
+    }
+    VD_CK(cudaDeviceSynchronize());
+    *flags = vdi::chk_flags_score(clear != 0) | vdi::chk_flags_ga(clear != 0);
+    return 1;
+#else
+    (void)clear;
+    *flags = 0;
+    return 0;
+#endif
 }
 
 int vd_device_count(int *count)

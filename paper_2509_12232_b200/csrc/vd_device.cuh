@@ -32,11 +32,69 @@
 
 namespace vd {
 
+/* ---- checked build (libvdb200_checked.so, -DVD_CHECKED) ------------------------------
+ * compute-sanitizer is closed on this pool, so the library carries its own checks:
+ *   VD_CHK(cond, site)  bounds / invariant checks; a failure sets bit `site` of a
+ *                       per-translation-unit device flag word (no trap: the run goes on
+ *                       and the host reads the flags, vd_debug_check_flags)
+ *   vd_poison_smem()    every kernel fills its dynamic shared memory with 0xFF bytes
+ *                       (NaN floats / -1 ints) before staging, so a read of a shared word
+ *                       no stage wrote shows up as a NaN result
+ *   VD_JITTER(k)        each warp sleeps a hashed 0-2 us at phase boundaries, so two
+ *                       warps that race on shared memory without a barrier between them
+ *                       see a different interleaving than in the production build; the
+ *                       results must stay bit-identical (tests/test_gpu_checked.py)
+ * In the production build all three compile to nothing. */
+enum {
+    VD_SITE_MAP = 0,     /* grid map index in [0, n_maps) */
+    VD_SITE_ATOM = 1,    /* atom index (torsion axis, fragment member, pair end) < n_atoms */
+    VD_SITE_FRAG = 2,    /* fragment slot inside the staged fragment list */
+    VD_SITE_SMEM = 3,    /* the launch's dynamic shared memory covers the layout */
+    VD_SITE_CELL = 4,    /* gather cell inside the grid */
+    VD_SITE_POP = 5,     /* GA individual index < pop */
+    VD_SITE_TILE = 6,    /* pair index inside the shared pair tile */
+};
+#ifdef VD_CHECKED
+static __device__ unsigned int g_vd_chk_flags;
+#define VD_CHK(cond, site)                                                        \
+    do {                                                                          \
+        if (!(cond)) atomicOr(&::vd::g_vd_chk_flags, 1u << (site));               \
+    } while (0)
+__device__ __forceinline__ unsigned dyn_smem_bytes()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void vd_poison_smem(unsigned char *smem, unsigned bytes)
+{
+    VD_CHK(bytes <= dyn_smem_bytes(), VD_SITE_SMEM);
+    const unsigned n = dyn_smem_bytes() / 4u;
+    for (unsigned k = threadIdx.x; k < n; k += blockDim.x) reinterpret_cast<unsigned *>(smem)[k] = 0xffffffffu;
+    __syncthreads();
+}
+__device__ __forceinline__ void vd_jitter(unsigned k)
+{
+    unsigned h = (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu) ^ (k * 0xC2B2AE35u);
+    h ^= h >> 13;
+    h *= 0x27D4EB2Fu;
+    h ^= h >> 16;
+    __nanosleep(h & 2047u);
+}
+#define VD_JITTER(k) ::vd::vd_jitter(k)
+#define VD_POISON(smem, bytes) ::vd::vd_poison_smem((smem), (bytes))
+#else
+#define VD_CHK(cond, site) ((void)0)
+#define VD_JITTER(k) ((void)0)
+#define VD_POISON(smem, bytes) ((void)0)
+#endif
+
 constexpr int kTile = 256;            /* pairs per streamed tile / fp32 partial (multiple of 8) */
 constexpr int kResidentPairs = 2048;  /* pair lists up to this stay resident in shared memory */
 
 struct GridView {
     const float *maps;      /* (n_maps, nx, ny, nz) */
+    int n_maps;
     int nx, ny, nz;
     int64_t mstride;        /* nx * ny * nz */
     float lo0, lo1, lo2, hi0, hi1, hi2, spacing;
@@ -95,9 +153,15 @@ __device__ __forceinline__ LigView stage_topology(const LigView &L, unsigned cha
         int4 r = __ldg(&L.tors[i]);
         r.z -= f0;
         r.w -= f0;
+        VD_CHK(r.x >= 0 && r.x < L.n_atoms && r.y >= 0 && r.y < L.n_atoms, VD_SITE_ATOM);
+        VD_CHK(r.z >= 0 && r.z <= r.w && r.w <= nf, VD_SITE_FRAG);
         t[i] = r;
     }
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) f[i] = __ldg(&L.frag[f0 + i]);
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        f[i] = __ldg(&L.frag[f0 + i]);
+        VD_CHK(f[i] >= 0 && f[i] < L.n_atoms, VD_SITE_ATOM);
+    }
+    VD_CHK(L.n_torsions == 0 || nf == L.n_frag, VD_SITE_FRAG);
     V.atom = a;
     V.atom2 = a2;
     V.tors = t;
@@ -227,6 +291,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
     const float2 ONE = f2(one), NEG = f2(-one);
 #endif
 #define VD_X(k) X[(k) * NPP]
+    VD_JITTER(1);
     float2 M00, M01, M02, M10, M11, M12, M20, M21, M22, TX, TY, TZ;
     if (TPP == 1) {
         float m0[9], t0[3], m1[9], t1[3];
@@ -275,6 +340,7 @@ __device__ __forceinline__ void build_pose2(const LigView &L, const double *__re
     if (TPP > 1) __syncthreads();
     for (int t = 0; t < L.n_torsions; ++t) {
         const int4 tr = L.tors[t];
+        VD_JITTER(2 + t);
         float2 KX, KY, KZ, C, SN;
         if (TPP == 1) {
             const float2 ox = VD_S2(tr.x, 0), oy = VD_S2(tr.x, 1), oz = VD_S2(tr.x, 2);
@@ -420,6 +486,10 @@ __device__ __forceinline__ void cell_of(const GridView &G, float x, float y, flo
     g.fz = __fsub_rn(uz, (float)iz);
     idx = (ix * G.ny + iy) * G.nz + iz;
     zy = ((ix * G.nyp + (iy >> 1)) * G.nz + iz) * 2 + (iy & 1);
+    VD_CHK(!g.inb || ((int)ux == ix && (int)uy == iy && (int)uz == iz) ||
+               ux >= (float)(G.nx - 2) || uy >= (float)(G.ny - 2) || uz >= (float)(G.nz - 2),
+           VD_SITE_CELL);
+    VD_CHK(idx >= 0 && (int64_t)idx + (int64_t)G.ny * G.nz + G.nz + 1 < G.mstride, VD_SITE_CELL);
 }
 
 __device__ __forceinline__ void ld256(const float4 *p, float4 &lo, float4 &hi)
@@ -620,6 +690,7 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
         {
             const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
             const float4 *tz = type_map(G, __float_as_int(L.atom2[i].y));
+            VD_CHK(__float_as_int(L.atom2[i].y) >= 0 && __float_as_int(L.atom2[i].y) < G.n_maps, VD_SITE_MAP);
             int idx0, idx1, zy0, zy1;
             cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0, zy0);
             cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1, zy1);
@@ -656,6 +727,8 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
     if constexpr (LAY == 1 && !EXACT) return;
     const float *emap = G.maps + G.mstride * L.elec_map;
     const float *dmap = G.maps + G.mstride * L.desolv_map;
+    VD_CHK(L.elec_map >= 0 && L.elec_map < G.n_maps && L.desolv_map >= 0 && L.desolv_map < G.n_maps,
+           VD_SITE_MAP);
     /* z-pair loads and the out-of-box early return, atom loop not unrolled: unrolled x2 the
        z-pair gathers raised the score kernel to 168 registers (1 CTA/SM: cfg1 1.41 -> 2.09 ms)
        and cost the GA 7-16%; not unrolled, cfg4 GA 1,297 -> 1,600 ligands/s */
@@ -664,6 +737,7 @@ __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, cons
         const float4 a = L.atom[i];
         const float2 a2 = L.atom2[i];
         const float *tmap = G.maps + G.mstride * __float_as_int(a2.y);
+        VD_CHK(__float_as_int(a2.y) >= 0 && __float_as_int(a2.y) < G.n_maps, VD_SITE_MAP);
         const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
         const float t0 = atom_term<EXACT, true>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.x, y.x, z.x);
         const float t1 = atom_term<EXACT, true>(G, tmap, emap, dmap, a.w, a2.x, L.penalty, x.y, y.y, z.y);
@@ -837,12 +911,16 @@ template <bool EXACT, int NPP>
 __device__ __forceinline__ void stage_pairs(const LigView &L, const PairTile &T, int k0, int cnt)
 {
     for (int k = threadIdx.x; k < cnt; k += blockDim.x) {
+        VD_CHK(k < T.cap, VD_SITE_TILE);
         if (EXACT) {
             T.coef[k] = __ldg(&L.pcoef[k0 + k]);
             T.j[k] = (int)__ldg(&L.pij[k0 + k]);
+            VD_CHK((int)(__ldg(&L.pij[k0 + k]) & 0x7fff) < L.n_atoms &&
+                       (int)((__ldg(&L.pij[k0 + k]) >> 15) & 0x7fff) < L.n_atoms, VD_SITE_ATOM);
         } else {
             T.coef[k] = __ldg(&L.fcoef[k0 + k]);
             const int w = __ldg(&L.fij[k0 + k]);
+            VD_CHK((w & 0xffff) < L.n_atoms && (w >> 16) >= 0 && (w >> 16) < L.n_atoms, VD_SITE_ATOM);
             T.off[k] = make_int2(3 * NPP * (w & 0xffff), 3 * NPP * (w >> 16));
         }
     }
@@ -941,6 +1019,8 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
                 for (int r = 0; r < kPre; ++r) {
                     const int k = (int)threadIdx.x + r * NPP * TPP;
                     if (k < tcnt) {
+                        VD_CHK(k < T.cap && (pw[r] & 0xffff) < L.n_atoms && (pw[r] >> 16) < L.n_atoms,
+                               VD_SITE_TILE);
                         T.coef[k] = pc[r];
                         T.off[k] = make_int2(3 * NPP * (pw[r] & 0xffff), 3 * NPP * (pw[r] >> 16));
                     }
@@ -985,6 +1065,7 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
        The GA does not split (7,022 vs 8,621 ligands/s): it pipelines its gathers instead. */
     constexpr int NI = TPP * VD_ROLE_NI8 / 8 > 0 ? TPP * VD_ROLE_NI8 / 8 : 1;
     constexpr int NA = TPP - NI > 0 ? TPP - NI : 1;
+    VD_JITTER(100);
     if (SPLIT && !EXACT && TPP >= 4 && NI < TPP && T.resident) {
         /* balance the two roles with the measured cost ratio of one atom's gathers to one
            pair (kSplitR): the pair subs also take the last xa atoms, or the gather subs the
@@ -1025,6 +1106,7 @@ __device__ __forceinline__ void reduce_subs(double *red, int pp, int sub, double
                                             double &a0, double &a1)
 {
     if (TPP == 1) return;
+    VD_JITTER(101);
     __syncthreads();
     red[(0 * TPP + sub) * NPP + pp] = e0;
     red[(1 * TPP + sub) * NPP + pp] = e1;

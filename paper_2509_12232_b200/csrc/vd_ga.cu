@@ -115,6 +115,7 @@ __device__ void breed_child(const GaDev &P, int G, const double *cur, const floa
         for (int j = 0; j < k; ++j) {
             const int idx = (int)vd_below(vd_words_get(&W, r * k + j),
                                           (uint64_t)P.pop);
+            VD_CHK(idx >= 0 && idx < P.pop, VD_SITE_POP);
             if (best < 0 || fit[idx] < fit[best]) best = idx;
         }
         win[r] = best;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(NPP *TPP, LAY == 3 ? 3 : ga_minb(NPP *TPP)) ga
 {
     constexpr int B = NPP * TPP;
     extern __shared__ __align__(16) unsigned char smem[];
+    VD_POISON(smem, lay.base.bytes);
     const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     const PairTile Tl = pair_tile(smem, lay.base);
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(NPP *TPP, LAY == 3 ? 3 : ga_minb(NPP *TPP)) ga
             }
             __syncthreads();
             const int idx = block_argmin(fit, nullptr, pop, s_idx, s_val);
+            VD_CHK(idx >= 0 && idx < pop, VD_SITE_POP);
             const float fb = fit[idx];
             const bool better = !have || fb < best_total;  /* strict '<' (vd/ga.py:217) */
             if (better) {
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(NPP *TPP, LAY == 3 ? 3 : ga_minb(NPP *TPP)) ga
                 for (int g = threadIdx.x; g < G; g += B) nxt[(size_t)e * G + g] = cur[(size_t)s_best * G + g];
                 __syncthreads();
             }
+            VD_JITTER(200);
             for (int c = threadIdx.x; c < pop - P.elitism; c += B)
                 breed_child(P, G, cur, fit, gen, c, k0, k1, nxt + (size_t)(P.elitism + c) * G);
             __syncthreads();
@@ -299,6 +303,11 @@ static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const 
     const int ctas = std::max(1, std::min(count, std::max(1, per_sm) * sms));
     e = cudaMallocAsync((void **)gene_buf, sizeof(double) * (size_t)ctas * 2 * P.pop * gmax, st);
     if (e != cudaSuccess) return e;
+#ifdef VD_CHECKED
+    /* poison the gene double buffers: an individual read before it is written is NaN */
+    e = cudaMemsetAsync(*gene_buf, 0xff, sizeof(double) * (size_t)ctas * 2 * P.pop * gmax, st);
+    if (e != cudaSuccess) return e;
+#endif
     k<<<ctas, NPP * TPP, bytes, st>>>(Gv, d_ligs, d_order, count, P, seed, base, d_work, *gene_buf,
                                       gmax, lay, out);
     ++vdi::g_launches;
@@ -404,6 +413,33 @@ __global__ void ga_breed_probe_kernel(GaDev P, int T, const double *cur, const f
 }  // namespace vd
 
 using vdi::set_error;
+
+namespace vd {
+__global__ void chk_selftest_ga_kernel(int bad) { VD_CHK(bad == 0, VD_SITE_POP); }
+}  // namespace vd
+
+namespace vdi {
+void chk_selftest_ga()
+{
+    vd::chk_selftest_ga_kernel<<<1, 32>>>(1);
+}
+
+unsigned chk_flags_ga(bool clear)
+{
+#ifdef VD_CHECKED
+    unsigned v = 0;
+    cudaMemcpyFromSymbol(&v, vd::g_vd_chk_flags, sizeof v);
+    if (clear) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(vd::g_vd_chk_flags, &z, sizeof z);
+    }
+    return v;
+#else
+    (void)clear;
+    return 0;
+#endif
+}
+}  // namespace vdi
 
 static vd::GaDev ga_dev(const vd_ga_params *p)
 {

@@ -54,6 +54,11 @@ vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map);
  * must not lower the limit another thread's launch of the same kernel relies on. */
 cudaError_t raise_smem_limit(const void *kernel, unsigned bytes);
 bool make_packed(vd_grid *g);
+/* checked build: the device check-flag word of each translation unit (0 otherwise) */
+unsigned chk_flags_score(bool clear);
+unsigned chk_flags_ga(bool clear);
+void chk_selftest_score();  /* raise one flag per translation unit (checked build) */
+void chk_selftest_ga();
 
 }  // namespace vdi
 

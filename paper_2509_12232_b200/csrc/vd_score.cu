@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
                                                          float *__restrict__ total)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    VD_POISON(smem, lay.bytes);
     const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
     float2 *S = reinterpret_cast<float2 *>(smem) + pp;
     const PairTile T = pair_tile(smem, lay);
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(NPP *TPP) pose_kernel(LigView Lg, const double
                                                         float one, float *__restrict__ out)
 {
     extern __shared__ __align__(16) unsigned char smem[];
+    VD_POISON(smem, lay.bytes);
     const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
     const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
                                      lay.topo_frag);
@@ -281,3 +283,30 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
 }
 
 }  // namespace vd
+
+namespace vd {
+__global__ void chk_selftest_score_kernel(int bad) { VD_CHK(bad == 0, VD_SITE_TILE); }
+}  // namespace vd
+
+namespace vdi {
+void chk_selftest_score()
+{
+    vd::chk_selftest_score_kernel<<<1, 32>>>(1);
+}
+
+unsigned chk_flags_score(bool clear)
+{
+#ifdef VD_CHECKED
+    unsigned v = 0;
+    cudaMemcpyFromSymbol(&v, vd::g_vd_chk_flags, sizeof v);
+    if (clear) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(vd::g_vd_chk_flags, &z, sizeof z);
+    }
+    return v;
+#else
+    (void)clear;
+    return 0;
+#endif
+}
+}  // namespace vdi

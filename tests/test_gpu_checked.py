@@ -1,0 +1,57 @@
+"""Memory and race checking without compute-sanitizer (closed on this pool).
+
+tools/sanitize_case.py drives every hot kernel shape (score TPP 1/4/8 with resident and
+streamed pair tiles and the role split, pose TPP 1/4/8, GA fast packed / plain / exact and
+concurrent bucket launches, grid build, MUGD transpose) twice, in separate processes:
+  * with the production library, and
+  * with libvdb200_checked.so (-DVD_CHECKED): device bounds and invariant checks on map
+    indices, atom / fragment / pair indices, gather cells, GA individual indices and the
+    dynamic shared-memory size; shared memory and the GA's gene buffers poisoned with NaN
+    before use (a read of a word no stage wrote turns a result into NaN); and a hashed
+    per-warp sleep at every phase boundary (a shared-memory race without a barrier then
+    sees another interleaving).
+Pass: no check flag raised, and every output of the checked run bit-identical to the
+production run.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+CHECKED = ROOT / "paper_2509_12232_b200" / "libvdb200_checked.so"
+
+
+def _run(tmp_path, lib=None):
+    out = tmp_path / ("checked.npz" if lib else "prod.npz")
+    env = dict(os.environ)
+    env.pop("VD_LIB", None)
+    if lib:
+        env["VD_LIB"] = str(lib)
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "sanitize_case.py"), str(out)],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-3000:])
+    return r.stdout, np.load(out)
+
+
+def test_checked_build_raises_no_flags_and_matches_production(tmp_path):
+    if not CHECKED.exists():
+        pytest.fail("libvdb200_checked.so not built: run __graft_entry__.build()")
+    log, chk = _run(tmp_path, CHECKED)
+    assert "checked_build=1 flags=0x0 selftest=0x60" in log, log  # no failure; flags do fire
+    _, prod = _run(tmp_path)
+    assert sorted(chk.files) == sorted(prod.files)
+    bad = [k for k in prod.files
+           if not np.array_equal(np.ascontiguousarray(prod[k]).view(np.uint8),
+                                 np.ascontiguousarray(chk[k]).view(np.uint8))]
+    assert not bad, bad
+    nan = [k for k in chk.files if chk[k].dtype.kind == "f" and np.isnan(chk[k]).any()]
+    assert not nan, nan

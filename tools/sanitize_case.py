@@ -1,13 +1,15 @@
-"""Small invocations of every hot kernel shape for compute-sanitizer (memcheck, racecheck,
-synccheck, initcheck: one tool per gpurun call).  No torch: the library through ctypes.
+"""Small invocations of every hot kernel shape, with all outputs saved, for the checked-
+build comparison (tests/test_gpu_checked.py; compute-sanitizer is closed on this pool).
 
   score_kernel  TPP 4 role split (cfg1 fixture, 40 atoms, resident pairs), TPP 8 with
-                streamed pair tiles (128-atom fixture), TPP 1 exact; z-pair, brick and
-                plain grid layouts; host-buffer pipeline path
+                streamed pair tiles (128-atom fixture), TPP 1 exact; yz-brick, z-pair
+                and plain grid layouts; the host-buffer pipeline path
   pose_kernel   TPP 1 / 4 / 8
-  ga_kernel     fast packed (incl. the 3-CTA r3 variant), fast plain, exact
-  grid_kernel   small device grid build
-Usage: compute-sanitizer --tool memcheck python tools/sanitize_case.py
+  ga_kernel     fast packed, fast plain, exact, several buckets at once (incl. the
+                3-CTA r3 variant for <= 32-atom buckets)
+  grid_kernel   a small device grid build; MUGD load (transpose kernel)
+Usage: [VD_LIB=.../libvdb200_checked.so] python tools/sanitize_case.py OUT.npz
+Prints the checked build's device flag word (0 = no bounds/invariant failure).
 """
 
 from __future__ import annotations
@@ -20,17 +22,20 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
+import ctypes  # noqa: E402
+
 import numpy as np  # noqa: E402
 
 import fixtures as fx  # noqa: E402
 from paper_2509_12232_b200 import _abi, gridmaps, hostprep, synth  # noqa: E402
 from paper_2509_12232_b200.backend import CudaBackend  # noqa: E402
 from paper_2509_12232_b200.context import prepare_context  # noqa: E402
-from paper_2509_12232_b200.ga import GaConfig, dock, _run  # noqa: E402
+from paper_2509_12232_b200.ga import GaConfig, _run, dock  # noqa: E402
 
 
-def main():
+def main(out_path):
     _abi.ensure_device(0)
+    out = {}
     for layout, env in (("brick", {"VD_BRICK_BUDGET_MB": "100000"}),
                         ("zpair", {"VD_BRICK_BUDGET_MB": "0"}), ("plain", {"VD_NO_PACK": "1"})):
         os.environ.update(env)
@@ -40,35 +45,45 @@ def main():
             ctx = prepare_context(c["topo"], g2, table=fx.TABLE)
             for mode in ("fast", "exact"):
                 b = CudaBackend(mode=mode, device=0)
-                b.score_population_arrays(c["genes"][:n], ctx)
-            grid, ligs = CudaBackend(mode="fast", device=0).prepared(ctx)
+                for k, v in zip("eat", b.score_population_arrays(c["genes"][:n], ctx)):
+                    out[f"{layout}_{name}_{mode}_score_{k}"] = v
+            _, ligs = CudaBackend(mode="fast", device=0).prepared(ctx)
             for tpp in (4, 8):
-                _abi.debug_pose_genes(ligs, 0, c["genes"][:n], tpp)
-            CudaBackend(mode="fast", device=0).pose_population(c["genes"][:n], ctx)
+                out[f"{layout}_{name}_pose{tpp}"] = _abi.debug_pose_genes(ligs, 0, c["genes"][:n], tpp)
+            out[f"{layout}_{name}_pose1"] = CudaBackend(mode="fast", device=0).pose_population(
+                c["genes"][:n], ctx)
             for mode in ("fast", "exact"):
-                dock(c["topo"], g2, GaConfig(population_size=40, generations=2, seed=1),
-                     backend=CudaBackend(mode=mode, device=0), context=ctx)
+                r = dock(c["topo"], g2, GaConfig(population_size=40, generations=3, seed=1),
+                         backend=CudaBackend(mode=mode, device=0), context=ctx)
+                out[f"{layout}_{name}_{mode}_ga_genes"] = r.best_genotype
+                out[f"{layout}_{name}_{mode}_ga_trace"] = r.trace
         for k in env:
             del os.environ[k]
-    # r3 variant + multi-bucket concurrent launches on a small cfg2-like batch
-    c = fx.pop_case("cfg1")
+    # several GA buckets at once (concurrent bucket launches, r3 variant) on a cfg2 batch
+    spec = gridmaps.GridSpec.centered((0.0, 0.0, 0.0), (40, 40, 40), 0.375)
+    gset = gridmaps.build_grid_maps(synth.make_protein(5, 1500), spec, synth.CONFIGS[2].probe_types)
+    out["grid_maps_sample"] = np.stack([gset.maps[l][::7, ::5, ::3] for l in gset.maps])
     b = CudaBackend(mode="fast", device=0)
-    grid = b._grid_for_set(c["grid"])
-    batch = hostprep.TopologyBatch.synth(2, 0, 12)
-    try:
-        arrays = hostprep.prepare_batch(batch, grid.labels, table=fx.TABLE)
-        lset = hostprep.ligand_set(arrays)
-        s = c["grid"].spec
-        _run(grid, lset, 0, 12, GaConfig(population_size=64, generations=2,
-                                         translation_bounds=(s.origin, s.upper)),
+    grid = b._grid_for_set(gset)
+    batch = hostprep.TopologyBatch.synth(2, 0, 40)
+    arrays = hostprep.prepare_batch(batch, grid.labels)
+    lset = hostprep.ligand_set(arrays)
+    r = _run(grid, lset, 0, 40, GaConfig(population_size=64, generations=3,
+                                         translation_bounds=(spec.origin, spec.upper)),
              0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
-    except ValueError:
-        pass
-    # device grid builder
-    prot = synth.make_protein(3, 300)
-    gridmaps.build_grid_maps(prot, gridmaps.GridSpec.centered((0, 0, 0), (9, 9, 9), 0.8), ["C", "HD"])
-    print("sanitize case done")
+    for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
+        out[f"batch_ga_{k}"] = v
+    mg = gridmaps.load_grid_set(fx.GOLDEN / "ref_grid_odd.mugd")
+    out["mugd_odd"] = mg.device_grid.download()
+    flags = ctypes.c_uint32(0)
+    checked = _abi.lib().vd_debug_check_flags(ctypes.byref(flags), 1)
+    selftest = ctypes.c_uint32(0)
+    _abi.lib().vd_debug_check_flags(ctypes.byref(selftest), -1)
+    np.savez(out_path, **out)
+    print(f"sanitize case done: checked_build={checked} flags=0x{flags.value:x} "
+          f"selftest=0x{selftest.value:x} arrays={len(out)}")
+    return 0 if flags.value == 0 else 3
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main(sys.argv[1] if len(sys.argv) > 1 else "sanitize_out.npz"))
