@@ -1052,12 +1052,63 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
     }
 }
 
+/* EXACT with TPP = 8 sub-threads per pose pair: the reference's lane-8 fp64 summation
+ * (scoring/simd.py:58-86: lane[k & 7] accumulates pairs k < 8*floor(n/8) in order, then a
+ * sequential tail, then s = lanes 0..7 in order + tail) with lane l on sub l.  Each lane is
+ * the same ordered fp64 chain as in the single-thread path, so the result is bit-identical;
+ * the 8 chains run in parallel instead of one thread walking all of them.  The lanes are
+ * combined through `red` ([4][TPP][NPP] doubles) by sub 0, which holds a0 / a1 on return
+ * (all CTA threads must call). */
+template <int NPP, int TPP>
+__device__ __forceinline__ void intra_exact_lanes(const LigView &L, const float2 *S, const PairTile &T,
+                                                  int sub, double *red, int pp, double &a0, double &a1)
+{
+    static_assert(TPP == 8, "one reference lane per sub");
+    const int n = L.n_pairs;
+    double l0 = 0.0, l1 = 0.0, tail0 = 0.0, tail1 = 0.0;
+    const int nblk8 = n & ~7;
+    const int step = T.resident ? (n > 0 ? n : 1) : T.cap;
+    for (int k0 = 0; k0 < n; k0 += step) {
+        const int cnt = min(step, n - k0);
+        if (!T.resident) {
+            __syncthreads();
+            stage_pairs<true, NPP>(L, T, k0, cnt);
+            __syncthreads();
+        }
+        const int cb = min(cnt, max(0, nblk8 - k0));  /* lane-blocked part of this tile */
+        for (int kb = 0; kb < cb; kb += 8) exact_pair<NPP>(S, T, kb + sub, L.cut2, l0, l1);
+        if (sub == 0)
+            for (int k = cb; k < cnt; ++k) exact_pair<NPP>(S, T, k, L.cut2, tail0, tail1);
+    }
+    __syncthreads();  /* red may alias the pair tile or the pose scratch */
+    red[(0 * TPP + sub) * NPP + pp] = l0;
+    red[(1 * TPP + sub) * NPP + pp] = l1;
+    __syncthreads();
+    if (sub == 0) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            s0 = __dadd_rn(s0, red[(0 * TPP + l) * NPP + pp]);
+            s1 = __dadd_rn(s1, red[(1 * TPP + l) * NPP + pp]);
+        }
+        a0 = __dadd_rn(s0, tail0);
+        a1 = __dadd_rn(s1, tail1);
+    }
+}
+
 /* inter + intra of both poses (all CTA threads must call) */
 template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
-                                        double &a0, double &a1)
+                                        double &a0, double &a1, double *red = nullptr, int pp = 0)
 {
+    if constexpr (EXACT && TPP > 1) {
+        /* inter: sub 0 alone, atoms in order (a sequential fp64 sum); intra: the 8 reference
+           lanes on the 8 subs (intra_exact_lanes).  Sub 0 ends holding all four sums. */
+        if (sub == 0) inter2<true, NPP, 1, false, LAY>(L, G, S, 0, 0, L.n_atoms, e0, e1);
+        intra_exact_lanes<NPP, TPP>(L, S, T, sub, red, pp, a0, a1);
+        return;
+    }
     /* SPLIT: the first NI = TPP * VD_ROLE_NI8 / 8 subs gather (L1TEX-bound) while the
        others run the pair sum (MUFU-bound) at the same time, so the two units overlap inside
        one CTA instead of only across CTAs.  Resident pair lists only (the streamed path has
@@ -1100,12 +1151,13 @@ __device__ __forceinline__ float total32(double inter, double intra, float tors)
     return __fadd_rn(__fadd_rn(__double2float_rn(inter), __double2float_rn(intra)), tors);
 }
 
-/* Sum per-sub partials (fast mode, TPP > 1) into sub 0; red: double[4][TPP][NPP]. */
-template <int NPP, int TPP>
+/* Sum per-sub partials (fast mode, TPP > 1) into sub 0; red: double[4][TPP][NPP].
+ * EXACT: sub 0 already holds the reference-ordered sums (energy2). */
+template <int NPP, int TPP, bool EXACT = false>
 __device__ __forceinline__ void reduce_subs(double *red, int pp, int sub, double &e0, double &e1,
                                             double &a0, double &a1)
 {
-    if (TPP == 1) return;
+    if (TPP == 1 || EXACT) return;
     VD_JITTER(101);
     __syncthreads();
     red[(0 * TPP + sub) * NPP + pp] = e0;

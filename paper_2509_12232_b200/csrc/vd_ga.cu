@@ -236,8 +236,9 @@ __global__ void __launch_bounds__(NPP *TPP, LAY == 3 ? 3 : ga_minb(NPP *TPP)) ga
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, (LAY == 3 ? 1 : LAY)>(L, Gv, S, Tl, sub, e0, e1, a0, a1);
-                reduce_subs<NPP, TPP>(red, pp, sub, e0, e1, a0, a1);
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, (LAY == 3 ? 1 : LAY)>(
+                    L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
+                reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
                     if (i1 < pop) { e64[i1] = e1; a64[i1] = a1; fit[i1] = total32(e1, a1, L.tors32); }
@@ -325,10 +326,12 @@ cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const Li
     return launch_ga_t<EX, N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, st,   \
                                  d_work, gene_buf, n_ctas)
     VD_G(true, 64, 1); VD_G(true, 32, 1); VD_G(true, 16, 1);
+    VD_G(true, 32, 8); VD_G(true, 16, 8);
     VD_G(false, 64, 1); VD_G(false, 32, 1); VD_G(false, 16, 1);
     VD_G(false, 64, 2); VD_G(false, 32, 2); VD_G(false, 16, 2);
     VD_G(false, 64, 4); VD_G(false, 32, 4); VD_G(false, 16, 4);
     VD_G(false, 32, 8); VD_G(false, 16, 8);
+    VD_G(false, 32, 16); VD_G(false, 16, 16);
 #undef VD_G
     return cudaErrorInvalidConfiguration;
 }
@@ -372,10 +375,12 @@ int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes, bool packed)
 #define VD_O(EX, N, T) \
     if (exact == EX && npp == N && tpp == T) return occ_t<EX, N, T>(bytes, packed)
     VD_O(true, 64, 1); VD_O(true, 32, 1); VD_O(true, 16, 1);
+    VD_O(true, 32, 8); VD_O(true, 16, 8);
     VD_O(false, 64, 1); VD_O(false, 32, 1); VD_O(false, 16, 1);
     VD_O(false, 64, 2); VD_O(false, 32, 2); VD_O(false, 16, 2);
     VD_O(false, 64, 4); VD_O(false, 32, 4); VD_O(false, 16, 4);
     VD_O(false, 32, 8); VD_O(false, 16, 8);
+    VD_O(false, 32, 16); VD_O(false, 16, 16);
 #undef VD_O
     return 0;
 }
@@ -587,7 +592,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         if (!exact)
             if (const char *ov = getenv("VD_GA_TPP")) {  /* tuning override */
                 const int v = atoi(ov);
-                if (v == 1 || v == 2 || v == 4 || v == 8) L.tpp = v;
+                if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) L.tpp = v;
             }
         /* pose-pairs per CTA: the candidate with most resident warps per SM
            (VD_GA_NPP forces one, for tuning) */

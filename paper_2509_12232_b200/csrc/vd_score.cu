@@ -60,11 +60,12 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     }
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
 #ifndef VD_TEST_STAGE
-    energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0, LAY>(L, G, S, T, sub, e0, e1, a0, a1);
+    energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0, LAY>(
+        L, G, S, T, sub, e0, e1, a0, a1, reinterpret_cast<double *>(smem + lay.red), pp);
 #else  /* (timing only) the pose stage alone */
     e0 = S[0].x; e1 = S[NPP].y;
 #endif
-    reduce_subs<NPP, TPP>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
+    reduce_subs<NPP, TPP, EXACT>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         if (p0 < P) {
             inter[p0] = e0;
@@ -117,7 +118,11 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
     const unsigned limit = 200 * 1024;
     /* threads per pose pair: more subs for larger ligands, where 12*N bytes of
        shared memory per pose leave few poses (and warps) per SM */
-    int t = exact ? 1 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 4 : 8));
+    /* EXACT: 8 subs = the reference's 8 summation lanes (intra_exact_lanes); VD_EXACT_TPP=1
+       keeps one thread per pose pair (A/B, and the bitwise cross-check of both paths) */
+    int t = exact ? 8 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 4 : 8));
+    if (exact)
+        if (const char *ov = getenv("VD_EXACT_TPP")) t = atoi(ov) == 1 ? 1 : 8;
     if (!exact)
         if (const char *ov = getenv("VD_TPP")) {  /* tuning override: 1, 2 or 4 */
             const int v = atoi(ov);
@@ -138,6 +143,7 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
     for (int pass = 0; pass < 2; ++pass)
         for (int n : {64, 32, 16}) {
             if (force_npp && n != force_npp) continue;
+            if (exact && t == 8 && n == 64) continue;  /* 512 threads: beyond the exact kernels' registers */
             const unsigned b = smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes;
             if (b <= (pass == 0 && !exact ? two_ctas : limit)) {
                 *npp = n;
@@ -237,6 +243,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
 #define VD_L(EX, N, T) \
     if (exact == EX && npp == N && tpp == T) return launch_t<EX, N, T>(G, L, g, p, P, ngenes, inter, intra, total, st)
     VD_L(true, 64, 1); VD_L(true, 32, 1); VD_L(true, 16, 1);
+    VD_L(true, 32, 8); VD_L(true, 16, 8);
     VD_L(false, 64, 1); VD_L(false, 32, 1); VD_L(false, 16, 1);
     VD_L(false, 64, 2); VD_L(false, 32, 2); VD_L(false, 16, 2);
     VD_L(false, 64, 4); VD_L(false, 32, 4); VD_L(false, 16, 4);

@@ -8,12 +8,13 @@ from paper_2509_12232_b200.backend import CudaBackend
 from paper_2509_12232_b200.ga import GaConfig, _run
 
 gens = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+mode = sys.argv[2] if len(sys.argv) > 2 else "fast"
 spec = synth.config_grid_spec(2)
 gset = gridmaps.build_grid_maps(synth.config_protein(2), spec, synth.CONFIGS[2].probe_types)
-b = CudaBackend("fast", 0)
+b = CudaBackend(mode, 0)
 grid = b._grid_for_set(gset)
 full = hostprep.TopologyBatch.synth(2, 0, 6000)
-keep = [l for l in range(len(full)) if 33 <= full.n_atoms[l] <= 48][:2048]
+keep = [l for l in range(len(full)) if 33 <= full.n_atoms[l] <= 48][:2048 if mode == "fast" else 512]
 topos = [full.topology(l) for l in keep]
 batch = hostprep.TopologyBatch.from_topologies(topos)
 lset = hostprep.ligand_set(hostprep.prepare_batch(batch, list(gset.maps)))
