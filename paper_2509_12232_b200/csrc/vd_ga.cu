@@ -183,8 +183,11 @@ constexpr int ga_minb(int threads)
 /* LAY: 1 packed grid, 2 plain grid, 3 packed grid with a 3-CTA register budget (168
  * registers instead of 245: for 32 x 4 tiles of small ligands, whose shared memory leaves
  * room for a third CTA that the full register budget does not) */
+#ifndef VD_GA_EXACT_MINB
+#define VD_GA_EXACT_MINB 2  /* resident CTAs the exact kernels are compiled for (cfg2 exact GA: 1 -> 2 CTAs at 128 registers, 1,017 -> 1,723 ligands/s) */
+#endif
 template <bool EXACT, int NPP, int TPP, int LAY>
-__global__ void __launch_bounds__(NPP *TPP, LAY == 3 ? 3 : ga_minb(NPP *TPP)) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+__global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : (LAY == 3 ? 3 : ga_minb(NPP *TPP))) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, int count,
                                                       GaDev P, uint64_t seed, int64_t base,
                                                       int *work, double *gene_buf, int gmax,

@@ -11,7 +11,7 @@ while [ $# -ge 2 ]; do
   ln -s "$ROOT/include" "$d/include"
   cp -r "$ROOT/paper_2509_12232_b200/csrc" "$d/pkg/csrc"
   rm -rf "$d/pkg/csrc/build"
-  make -s -j8 -C "$d/pkg/csrc" EXTRA="$flags" OUT="$d/libvdb200.so" > "$d/build.out" 2>&1 \
+  make -s -j8 -C "$d/pkg/csrc" EXTRA="$flags" OUT="$d/libvdb200.so" "$d/libvdb200.so" > "$d/build.out" 2>&1 \
     || { cat "$d/build.out"; exit 1; }
   echo "built $name ($flags)"
 done
