@@ -678,11 +678,31 @@ __device__ __forceinline__ float atom_term(const GridView &G, const float *__res
  * The kernels are instantiated per layout so that neither path's registers weigh on the
  * other (with both compiled in, the plain path's z-pair gathers took the score kernel from
  * 121 to 168 registers, 1 CTA/SM). */
-template <bool EXACT, int NPP, int TPP, bool PIPE, int LAY = 0>
+template <bool EXACT, int NPP, int TPP, bool PIPE, int LAY = 0, bool FLAT = false>
 __device__ __forceinline__ void inter2(const LigView &L, const GridView &G, const float2 *S,
                                        int sub, int ia, int ib, double &e0, double &e1)
 {
     if (LAY != 2 && G.yz != nullptr && !EXACT) {
+        if (FLAT) {
+            /* no gather state carried across atoms: inside a loop over pose tiles (the
+               persistent score kernel) the carried Gather pair set the register peak
+               (92 -> 148 registers for this stage alone) */
+            for (int i = ia + sub; i < ib; i += TPP) {
+                Gather c0, c1;
+                const float2 x = VD_S2(i, 0), y = VD_S2(i, 1), z = VD_S2(i, 2);
+                const float4 *tz = type_map(G, __float_as_int(L.atom2[i].y));
+                VD_CHK(__float_as_int(L.atom2[i].y) >= 0 && __float_as_int(L.atom2[i].y) < G.n_maps, VD_SITE_MAP);
+                int idx0, idx1, zy0, zy1;
+                cell_of(G, x.x, y.x, z.x, L.penalty, c0, idx0, zy0);
+                cell_of(G, x.y, y.y, z.y, L.penalty, c1, idx1, zy1);
+                issue_packed(G, tz, idx0, zy0, c0, true);
+                issue_packed(G, tz, idx1, zy1, c1, true);
+                const float q = L.atom[i].w, dsf = L.atom2[i].x;
+                e0 = __dadd_rn(e0, (double)finish_packed(c0, q, dsf, G.one));
+                e1 = __dadd_rn(e1, (double)finish_packed(c1, q, dsf, G.one));
+            }
+            return;
+        }
         const int n = ib;
         int i = ia + sub;
         if (i >= n) return;
@@ -1097,7 +1117,7 @@ __device__ __forceinline__ void intra_exact_lanes(const LigView &L, const float2
 }
 
 /* inter + intra of both poses (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0>
+template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0, bool FLAT = false>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
                                         double &a0, double &a1, double *red = nullptr, int pp = 0)
@@ -1131,18 +1151,18 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
         const unsigned px = ex < 0.f ? (unsigned)(-ex * kSplitR / (2.0f * (float)np) * 65536.0f) : 0u;
         const int acut = n - xa;
         if (sub < NI) {
-            inter2<EXACT, NPP, NI, PIPE, LAY>(L, G, S, sub, 0, acut, e0, e1);
+            inter2<EXACT, NPP, NI, PIPE, LAY, FLAT>(L, G, S, sub, 0, acut, e0, e1);
             if (px) intra2<EXACT, NPP, NA>(L, S, T, sub, a0, a1, 65536u - px + sub * px / NI,
                                            65536u - px + (sub + 1) * px / NI);
         } else {
             const int s = sub - NI;
             intra2<EXACT, NPP, NA>(L, S, T, s, a0, a1, s * (65536u - px) / NA,
                                    (s + 1) * (65536u - px) / NA);
-            if (acut < n) inter2<EXACT, NPP, NA, PIPE, LAY>(L, G, S, s, acut, n, e0, e1);
+            if (acut < n) inter2<EXACT, NPP, NA, PIPE, LAY, FLAT>(L, G, S, s, acut, n, e0, e1);
         }
         return;
     }
-    inter2<EXACT, NPP, TPP, PIPE, LAY>(L, G, S, sub, 0, L.n_atoms, e0, e1);
+    inter2<EXACT, NPP, TPP, PIPE, LAY, FLAT>(L, G, S, sub, 0, L.n_atoms, e0, e1);
     intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
 }
 

@@ -161,6 +161,16 @@ struct GaLayout {
     SmemLayout base;          /* pose tile + pair tiles (+ reduction) for the largest ligand */
     unsigned off_fit, off_e, off_a, off_taken;
     int r3 = 0;               /* host: launch the 3-CTA register-budget variant (LAY 3) */
+    int team = 1;             /* host: CTAs per ligand (ga_team_kernel when > 1) */
+};
+
+/* Per-team global state of ga_team_kernel (one team = `team` CTAs docking one ligand). */
+struct GaTeam {
+    double *genes;            /* [teams][2][pop][gmax] double-buffered population */
+    float *fit;               /* [teams][pop] */
+    double *e64, *a64;        /* [teams][pop] */
+    unsigned *bar;            /* [teams] arrival counters (zeroed at launch) */
+    int *lig;                 /* [teams] the ligand slot the team's leader fetched */
 };
 
 #ifndef VD_GA_MINB
@@ -285,6 +295,195 @@ __global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : (LAY == 3
     }
 }
 
+/* Team barrier over the `team` co-resident CTAs of one ligand: arrival counter in global
+ * memory, epoch kept per CTA (all CTAs of a team pass the same number of barriers).  The
+ * fences order each CTA's global writes (fitness, genes) before its arrival and the team's
+ * writes before the reads after the wait. */
+__device__ __forceinline__ void team_sync(unsigned *bar, unsigned team, unsigned &epoch)
+{
+    __syncthreads();
+    epoch += team;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+        while (*reinterpret_cast<volatile unsigned *>(bar) < epoch) __nanosleep(100);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+/* ga_kernel with one ligand's population split over a team of `lay.team` CTAs (rank r
+ * scores individuals [r*pop/team, (r+1)*pop/team) and breeds children [r*nc/team, ...)),
+ * so a batch with few ligands per SM still fills the GPU (BASELINE cfg4 at 8 GPUs: 250
+ * ligands per GPU, 148 one-CTA SMs).  Fitness and energies go through per-team global
+ * arrays, genes stay in a per-team global double buffer; two team barriers per
+ * generation.  Every CTA computes the selection from the full fitness array, so the
+ * decisions, the RNG draws (keyed by child index) and the results are bit-identical to
+ * ga_kernel's.  Launched cooperatively (all CTAs co-resident). */
+template <int NPP, int TPP, int LAY>
+__global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const LigView *__restrict__ ligs,
+                                                           const int *__restrict__ order, int count,
+                                                           GaDev P, uint64_t seed, int64_t base,
+                                                           int *work, GaTeam tm, int gmax,
+                                                           GaLayout lay, GaOut out)
+{
+    constexpr bool EXACT = false;
+    constexpr int B = NPP * TPP;
+    extern __shared__ __align__(16) unsigned char smem[];
+    VD_POISON(smem, lay.base.bytes);
+    const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
+    float2 *S = reinterpret_cast<float2 *>(smem) + pp;
+    const PairTile Tl = pair_tile(smem, lay.base);
+    double *red = reinterpret_cast<double *>(smem + lay.base.red);
+    float *fit = reinterpret_cast<float *>(smem + lay.off_fit);
+    unsigned char *taken = smem + lay.off_taken;
+    __shared__ int s_lig, s_best;
+    __shared__ int s_idx[33];
+    __shared__ float s_val[32];
+    const int pop = P.pop, team = lay.team;
+    const int tid = blockIdx.x / team, rank = blockIdx.x % team;
+    double *buf0 = tm.genes + (size_t)tid * 2 * pop * gmax, *buf1 = buf0 + (size_t)pop * gmax;
+    float *gfit = tm.fit + (size_t)tid * pop;
+    double *ge = tm.e64 + (size_t)tid * pop, *ga = tm.a64 + (size_t)tid * pop;
+    unsigned *bar = tm.bar + tid;
+    unsigned epoch = 0;
+    /* scored here: whole pose pairs (2k, 2k+1), as in ga_kernel -- the shared reciprocal
+       (VD_SHARED_RCP) makes a pose's fast energy depend on its pair partner */
+    const int pairs = (pop + 1) / 2;
+    const int i_lo = 2 * (rank * pairs / team), i_hi = min(pop, 2 * ((rank + 1) * pairs / team));
+    for (;;) {
+        if (rank == 0 && threadIdx.x == 0) tm.lig[tid] = atomicAdd(work, 1);
+        team_sync(bar, team, epoch);
+        if (threadIdx.x == 0) s_lig = *reinterpret_cast<volatile int *>(tm.lig + tid);
+        __syncthreads();
+        const int slot = s_lig;
+        if (slot >= count) break;
+        const int l = order ? order[slot] : slot;
+        const LigView L = stage_topology(ligs[l], smem, lay.base.topo_atom, lay.base.topo_atom2,
+                                         lay.base.topo_tors, lay.base.topo_frag);
+        stage_resident<EXACT, NPP>(L, Tl);
+        const int T = L.n_torsions, G = 7 + T;
+        const int nc = pop - P.elitism;
+        const int c_lo = rank * nc / team, c_hi = (rank + 1) * nc / team;  /* bred here */
+        const uint64_t k0 = seed, k1 = (uint64_t)(base + l);
+        double *cur = buf0, *nxt = buf1;
+        for (int i = i_lo + threadIdx.x; i < i_hi; i += B) init_individual(P, T, i, k0, k1, cur + (size_t)i * G);
+        float best_total = INFINITY;
+        bool have = false;
+        __syncthreads();
+        for (int gen = 0; gen <= P.generations; ++gen) {
+            for (int b0 = i_lo; b0 < i_hi; b0 += 2 * NPP) {
+                if (TPP > 1 && b0 > i_lo) __syncthreads();
+                const int i0 = b0 + 2 * pp, i1 = i0 + 1;
+                build_pose2<NPP, TPP>(L, cur + (size_t)min(i0, i_hi - 1) * G,
+                                      cur + (size_t)min(i1, i_hi - 1) * G, S, sub,
+                                      reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
+                if (TPP > 1) __syncthreads();
+                double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, LAY>(
+                    L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
+                reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
+                if (sub == 0) {
+                    if (i0 < i_hi) { ge[i0] = e0; ga[i0] = a0; gfit[i0] = total32(e0, a0, L.tors32); }
+                    if (i1 < i_hi) { ge[i1] = e1; ga[i1] = a1; gfit[i1] = total32(e1, a1, L.tors32); }
+                }
+            }
+            team_sync(bar, team, epoch);  /* every slice scored */
+            for (int i = threadIdx.x; i < pop; i += B) fit[i] = __ldcg(gfit + i);
+            __syncthreads();
+            const int idx = block_argmin(fit, nullptr, pop, s_idx, s_val);
+            VD_CHK(idx >= 0 && idx < pop, VD_SITE_POP);
+            const float fb = fit[idx];
+            const bool better = !have || fb < best_total;  /* strict '<' (vd/ga.py:217) */
+            if (better) {
+                if (rank == 0) {
+                    for (int g = threadIdx.x; g < G; g += B)
+                        out.best_genes[(size_t)l * out.gstride + g] = __ldcg(cur + (size_t)idx * G + g);
+                    if (threadIdx.x == 0) {
+                        out.best_total[l] = fb;
+                        out.best_inter[l] = __ldcg(ge + idx);
+                        out.best_intra[l] = __ldcg(ga + idx);
+                    }
+                }
+                best_total = fb;
+                have = true;
+            }
+            if (rank == 0 && out.trace && threadIdx.x == 0) out.trace[(size_t)l * (P.generations + 1) + gen] = fb;
+            if (gen == P.generations) break;
+            if (rank == 0) {  /* elites: first `elitism` of a stable ascending sort */
+                for (int i = threadIdx.x; i < pop; i += B) taken[i] = 0;
+                __syncthreads();
+                for (int e = 0; e < P.elitism; ++e) {
+                    const int ei = e == 0 ? idx : block_argmin(fit, taken, pop, s_idx, s_val);
+                    if (threadIdx.x == 0) { taken[ei] = 1; s_best = ei; }
+                    __syncthreads();
+                    for (int g = threadIdx.x; g < G; g += B) nxt[(size_t)e * G + g] = __ldcg(cur + (size_t)s_best * G + g);
+                    __syncthreads();
+                }
+            }
+            for (int c = c_lo + threadIdx.x; c < c_hi; c += B)
+                breed_child(P, G, cur, fit, gen, c, k0, k1, nxt + (size_t)(P.elitism + c) * G);
+            team_sync(bar, team, epoch);  /* the next generation is written */
+            double *t = cur; cur = nxt; nxt = t;
+        }
+        if (rank == 0 && threadIdx.x == 0) out.n_evals[l] = (int64_t)pop * (P.generations + 1);
+        __syncthreads();
+    }
+}
+
+/* One cooperative launch of the team kernel; `team` CTAs per ligand. */
+template <int NPP, int TPP>
+static cudaError_t launch_ga_team_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
+                                    int count, const GaDev &P, uint64_t seed, int64_t base, int gmax,
+                                    const GaLayout &lay, const GaOut &out, cudaStream_t st,
+                                    int *d_work, double **team_buf, int *n_ctas)
+{
+    auto k = ga_team_kernel<NPP, TPP, 2>;
+    if (Gv.yz != nullptr) k = ga_team_kernel<NPP, TPP, 1>;
+    const unsigned bytes = lay.base.bytes;
+    cudaError_t e = vdi::raise_smem_limit((const void *)k, bytes);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NPP * TPP, bytes);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int team = lay.team;
+    const int teams = std::max(1, std::min(count, std::max(1, per_sm) * sms / team));
+    const int ctas = teams * team;
+    /* genes (2 buffers) + fitness + e64 + a64 + barrier + ligand slot per team */
+    const size_t gbytes = sizeof(double) * (size_t)teams * 2 * P.pop * gmax;
+    const size_t fbytes = sizeof(float) * (size_t)teams * P.pop;
+    const size_t ebytes = sizeof(double) * (size_t)teams * P.pop;
+    const size_t total = gbytes + fbytes + 2 * ebytes + 2 * sizeof(unsigned) * teams + 64;
+    e = cudaMallocAsync((void **)team_buf, total, st);
+    if (e != cudaSuccess) return e;
+    char *p = reinterpret_cast<char *>(*team_buf);
+    GaTeam tm;
+    tm.genes = reinterpret_cast<double *>(p);
+    tm.e64 = reinterpret_cast<double *>(p + gbytes);
+    tm.a64 = reinterpret_cast<double *>(p + gbytes + ebytes);
+    tm.fit = reinterpret_cast<float *>(p + gbytes + 2 * ebytes);
+    tm.bar = reinterpret_cast<unsigned *>(p + gbytes + 2 * ebytes + fbytes);
+    tm.lig = reinterpret_cast<int *>(tm.bar + teams);
+    e = cudaMemsetAsync(tm.bar, 0, 2 * sizeof(unsigned) * teams, st);
+    if (e != cudaSuccess) return e;
+#ifdef VD_CHECKED
+    e = cudaMemsetAsync(tm.genes, 0xff, gbytes + fbytes + 2 * ebytes, st);
+    if (e != cudaSuccess) return e;
+#endif
+    GridView gv = Gv;
+    GaDev pd = P;
+    GaLayout ly = lay;
+    GaOut o = out;
+    void *args[] = {&gv, (void *)&d_ligs, (void *)&d_order, &count, &pd, &seed, &base, &d_work, &tm,
+                    &gmax, &ly, &o};
+    e = cudaLaunchCooperativeKernel((const void *)k, dim3(ctas), dim3(NPP * TPP), args, bytes, st);
+    ++vdi::g_launches;
+    *n_ctas = ctas;
+    return e;
+}
+
 template <bool EXACT, int NPP, int TPP>
 static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
                                int count, const GaDev &P, uint64_t seed, int64_t base, int gmax,
@@ -324,6 +523,14 @@ cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const Li
                       int gmax, const GaLayout &lay, const GaOut &out, cudaStream_t st,
                       int *d_work, double **gene_buf, int *n_ctas)
 {
+    if (!exact && lay.team > 1) {
+        if (npp == 32 && tpp == 8)
+            return launch_ga_team_t<32, 8>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out,
+                                           st, d_work, gene_buf, n_ctas);
+        if (npp == 16 && tpp == 8)
+            return launch_ga_team_t<16, 8>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out,
+                                           st, d_work, gene_buf, n_ctas);
+    }
 #define VD_G(EX, N, T)                                                                             \
     if (exact == EX && npp == N && tpp == T)                                                       \
     return launch_ga_t<EX, N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, st,   \
@@ -634,9 +841,25 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
             return -1;
         }
+        /* teams: with few ligands per CTA slot (BASELINE cfg4 at 8 GPUs: 250 ligands on 148
+           one-CTA SMs, 1.7 waves) a ligand's population is split over `team` CTAs so the batch
+           still fills the GPU in whole waves (ga_team_kernel; results are bit-identical).
+           VD_GA_TEAM=n forces a team size (1 = never split). */
+        L.lay.team = 1;
+        if (!exact && L.tpp == 8 && (L.npp == 32 || L.npp == 16)) {
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            const int per_sm = std::max(1, vd::ga_occupancy(false, L.npp, L.tpp, L.lay.base.bytes, gv.yz != nullptr));
+            const int slots = per_sm * sms;
+            int team = 1;
+            while (team < 8 && (double)v.size() * team / slots < 6.0 && v.size() * team < (size_t)(8 * slots)) team *= 2;
+            if (const char *ov = getenv("VD_GA_TEAM")) team = std::max(1, std::min(8, atoi(ov)));
+            L.lay.team = team;
+        }
         if (getenv("VD_VERBOSE"))
-            fprintf(stderr, "[vd] ga bucket <=%d atoms: %zu ligands, npp=%d tpp=%d smem=%u warps/sm=%d\n",
-                    kBucketEdge[b], v.size(), L.npp, L.tpp, L.lay.base.bytes, best_warps);
+            fprintf(stderr, "[vd] ga bucket <=%d atoms: %zu ligands, npp=%d tpp=%d smem=%u warps/sm=%d team=%d\n",
+                    kBucketEdge[b], v.size(), L.npp, L.tpp, L.lay.base.bytes, best_warps, L.lay.team);
         unsigned off = L.lay.base.extra;
         L.lay.off_e = off;
         off += 8u * p->pop;

@@ -26,6 +26,12 @@
 
 namespace vd {
 
+#ifndef VD_SCORE_PERSIST
+#define VD_SCORE_PERSIST 0  /* 1: a CTA walks pose tiles (staging once), flat gathers */
+#endif
+#ifndef VD_INTER_FLAT
+#define VD_INTER_FLAT VD_SCORE_PERSIST
+#endif
 template <bool EXACT, int NPP, int TPP, int LAY>
 __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
                                                          const double *__restrict__ genes,
@@ -44,38 +50,47 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
                                      lay.topo_frag);
     stage_resident<EXACT, NPP>(L, T);
     __syncthreads();
-    const int64_t p0 = ((int64_t)blockIdx.x * NPP + pp) * 2, p1 = p0 + 1;
-    const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;  /* tail: duplicate, drop */
-    if (genes) {
-        build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
-                              reinterpret_cast<float *>(smem + lay.scratch) + pp, G.one);
-        if (TPP > 1) __syncthreads();
-    } else {
-        const int n = L.n_atoms;
-        const float *s0 = poses + q0 * 3 * n, *s1 = poses + q1 * 3 * n;
-        for (int i = sub; i < n; i += TPP)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) VD_S2(i, c) = f2(s0[c * n + i], s1[c * n + i]);
-        if (TPP > 1) __syncthreads();
-    }
-    double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-#ifndef VD_TEST_STAGE
-    energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0, LAY>(
-        L, G, S, T, sub, e0, e1, a0, a1, reinterpret_cast<double *>(smem + lay.red), pp);
-#else  /* (timing only) the pose stage alone */
-    e0 = S[0].x; e1 = S[NPP].y;
+#if VD_SCORE_PERSIST
+    const int64_t n_tiles = (P + 2 * NPP - 1) / (2 * NPP);
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        if (tile != blockIdx.x) __syncthreads();  /* tile, scratch and reduction free */
+#else
+    {
+        const int64_t tile = blockIdx.x;
 #endif
-    reduce_subs<NPP, TPP, EXACT>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
-    if (sub == 0) {
-        if (p0 < P) {
-            inter[p0] = e0;
-            intra[p0] = a0;
-            if (total) total[p0] = total32(e0, a0, L.tors32);
+        const int64_t p0 = (tile * NPP + pp) * 2, p1 = p0 + 1;
+        const int64_t q0 = p0 < P ? p0 : P - 1, q1 = p1 < P ? p1 : P - 1;  /* tail: duplicate, drop */
+        if (genes) {
+            build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
+                                  reinterpret_cast<float *>(smem + lay.scratch) + pp, G.one);
+            if (TPP > 1) __syncthreads();
+        } else {
+            const int n = L.n_atoms;
+            const float *s0 = poses + q0 * 3 * n, *s1 = poses + q1 * 3 * n;
+            for (int i = sub; i < n; i += TPP)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) VD_S2(i, c) = f2(s0[c * n + i], s1[c * n + i]);
+            if (TPP > 1) __syncthreads();
         }
-        if (p1 < P) {
-            inter[p1] = e1;
-            intra[p1] = a1;
-            if (total) total[p1] = total32(e1, a1, L.tors32);
+        double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
+#ifndef VD_TEST_STAGE
+        energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0, LAY, VD_INTER_FLAT != 0>(
+            L, G, S, T, sub, e0, e1, a0, a1, reinterpret_cast<double *>(smem + lay.red), pp);
+#else  /* (timing only) the pose stage alone */
+        e0 = S[0].x; e1 = S[NPP].y;
+#endif
+        reduce_subs<NPP, TPP, EXACT>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
+        if (sub == 0) {
+            if (p0 < P) {
+                inter[p0] = e0;
+                intra[p0] = a0;
+                if (total) total[p0] = total32(e0, a0, L.tors32);
+            }
+            if (p1 < P) {
+                inter[p1] = e1;
+                intra[p1] = a1;
+                if (total) total[p1] = total32(e1, a1, L.tors32);
+            }
         }
     }
 }
@@ -169,7 +184,7 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
        launches once per pipeline chunk, so it is done once per (device, shared-memory size) */
     /* (the function attributes are per kernel: the dynamic shared-memory limit only ever
        grows, and the carveout is re-applied when another shape changed it) */
-    struct Setup { int dev; const void *fn; unsigned bytes; int pct; };
+    struct Setup { int dev; const void *fn; unsigned bytes; int pct; int ctas; };
     /* process-wide (the attributes are): threads scoring different ligands concurrently must
        never lower the limit another thread's launch relies on */
     static std::mutex mu;
@@ -190,7 +205,7 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
                 if (e != cudaSuccess) return e;
                 *carve = x.pct;
             }
-            const int64_t blocks = (P + 2 * NPP - 1) / (2 * NPP);
+            const int64_t blocks = std::min<int64_t>((P + 2 * NPP - 1) / (2 * NPP), x.ctas);
             k<<<(unsigned)blocks, NPP * TPP, lay.bytes, st>>>(G, L, genes, poses, P, ngenes, lay,
                                                                 inter, intra, total);
             ++vdi::g_launches;
@@ -218,9 +233,20 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
     if (e != cudaSuccess) return e;
     *carve = pct;
-    if (done_setups.size() < 64) done_setups.push_back({cur_dev, (const void *)k, lay.bytes, pct});
+    /* persistent build: one CTA per resident slot (VD_SCORE_CTAS_PER_SM overrides) */
+    int ctas = INT32_MAX;
+#if VD_SCORE_PERSIST
+    {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int per_sm = want;
+        if (const char *c = getenv("VD_SCORE_CTAS_PER_SM")) per_sm = std::max(1, atoi(c));
+        ctas = per_sm * sms;
+    }
+#endif
+    if (done_setups.size() < 64) done_setups.push_back({cur_dev, (const void *)k, lay.bytes, pct, ctas});
     const int64_t per_cta = 2 * NPP;
-    const int64_t blocks = (P + per_cta - 1) / per_cta;
+    const int64_t blocks = std::min<int64_t>((P + per_cta - 1) / per_cta, ctas);
     if (getenv("VD_VERBOSE"))
         fprintf(stderr, "[vd] score_kernel<%d,%d,%d> N=%d P=%d smem=%u ctas/sm=%d carveout=%d%%\n",
                 (int)EXACT, NPP, TPP, L.n_atoms, L.n_pairs, lay.bytes, want, pct);

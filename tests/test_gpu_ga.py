@@ -287,3 +287,33 @@ def test_r3_register_budget_variant_is_bit_identical(cuda, monkeypatch):
     b = run()
     for x, y in zip(a, b):
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+
+
+@pytest.mark.parametrize("team", ["2", "4", "8"])
+def test_team_split_ga_is_bit_identical(cuda, team, monkeypatch):
+    """Large ligands in small batches split one ligand's population over a team of CTAs
+    (ga_team_kernel: fitness through global memory, two team barriers per generation).
+    Selection, RNG and scoring are unchanged, so every output equals the one-CTA GA's."""
+    from paper_2509_12232_b200 import _abi, gridmaps, hostprep, synth
+    from paper_2509_12232_b200.ga import GaConfig, _run
+
+    spec = gridmaps.GridSpec.centered((0.0, 0.0, 0.0), (56, 56, 56), 0.375)
+    gset = gridmaps.build_grid_maps(synth.make_protein(11, 2500, half_extent=14.0), spec,
+                                    synth.CONFIGS[4].probe_types)
+    grid = cuda["fast"]._grid_for_set(gset)
+    batch = hostprep.TopologyBatch.synth(4, 3, 10)
+    lset = hostprep.ligand_set(hostprep.prepare_batch(batch, grid.labels))
+    gmax = 7 + int(batch.n_torsions.max())
+    # pop 100: slices of 100 / team individuals, odd tile tails; elitism 3 crosses slices
+    ga = GaConfig(population_size=100, generations=6, elitism_count=3,
+                  translation_bounds=(spec.origin, spec.upper))
+
+    def run(t):
+        monkeypatch.setenv("VD_GA_TEAM", t)
+        r = _run(grid, lset, 0, 10, ga, 9, 40, _abi.MODE_FAST, gmax)
+        monkeypatch.delenv("VD_GA_TEAM")
+        return r
+
+    one, split = run("1"), run(team)
+    for x, y in zip(one, split):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
