@@ -524,12 +524,12 @@ cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const Li
                       int *d_work, double **gene_buf, int *n_ctas)
 {
     if (!exact && lay.team > 1) {
-        if (npp == 32 && tpp == 8)
-            return launch_ga_team_t<32, 8>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out,
-                                           st, d_work, gene_buf, n_ctas);
-        if (npp == 16 && tpp == 8)
-            return launch_ga_team_t<16, 8>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out,
-                                           st, d_work, gene_buf, n_ctas);
+#define VD_T(N, T)                                                                                  \
+        if (npp == N && tpp == T)                                                                   \
+            return launch_ga_team_t<N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, \
+                                          st, d_work, gene_buf, n_ctas)
+        VD_T(32, 8); VD_T(16, 8); VD_T(32, 4); VD_T(16, 4);
+#undef VD_T
     }
 #define VD_G(EX, N, T)                                                                             \
     if (exact == EX && npp == N && tpp == T)                                                       \
@@ -842,11 +842,12 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             return -1;
         }
         /* teams: with few ligands per CTA slot (BASELINE cfg4 at 8 GPUs: 250 ligands on 148
-           one-CTA SMs, 1.7 waves) a ligand's population is split over `team` CTAs so the batch
-           still fills the GPU in whole waves (ga_team_kernel; results are bit-identical).
+           one-CTA SMs, 1.7 waves; a single dock: 1 ligand) a ligand's population is split over
+           `team` CTAs so the batch still fills the GPU in whole waves (ga_team_kernel; results
+           are bit-identical).
            VD_GA_TEAM=n forces a team size (1 = never split). */
         L.lay.team = 1;
-        if (!exact && L.tpp == 8 && (L.npp == 32 || L.npp == 16)) {
+        if (!exact && (L.tpp == 8 || L.tpp == 4) && (L.npp == 32 || L.npp == 16)) {
             int dev = 0, sms = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -856,6 +857,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             while (team < 8 && (double)v.size() * team / slots < 6.0 && v.size() * team < (size_t)(8 * slots)) team *= 2;
             if (const char *ov = getenv("VD_GA_TEAM")) team = std::max(1, std::min(8, atoi(ov)));
             L.lay.team = team;
+            if (team > 1) L.lay.r3 = 0;  /* the team kernel has no 3-CTA register variant */
         }
         if (getenv("VD_VERBOSE"))
             fprintf(stderr, "[vd] ga bucket <=%d atoms: %zu ligands, npp=%d tpp=%d smem=%u warps/sm=%d team=%d\n",

@@ -6,7 +6,8 @@ build comparison (tests/test_gpu_checked.py; compute-sanitizer is closed on this
                 and plain grid layouts; the host-buffer pipeline path
   pose_kernel   TPP 1 / 4 / 8
   ga_kernel     fast packed, fast plain, exact, several buckets at once (incl. the
-                3-CTA r3 variant for <= 32-atom buckets)
+                3-CTA r3 variant for <= 32-atom buckets); ga_team_kernel (6 cfg4
+                ligands: one ligand over 8 CTAs)
   grid_kernel   a small device grid build; MUGD load (transpose kernel)
 Usage: [VD_LIB=.../libvdb200_checked.so] python tools/sanitize_case.py OUT.npz
 Prints the checked build's device flag word (0 = no bounds/invariant failure).
@@ -73,6 +74,14 @@ def main(out_path):
              0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
     for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
         out[f"batch_ga_{k}"] = v
+    # large ligands in a small batch: the team kernel (a ligand's population over 8 CTAs)
+    b4 = hostprep.TopologyBatch.synth(4, 0, 6)
+    l4 = hostprep.ligand_set(hostprep.prepare_batch(b4, grid.labels))
+    r = _run(grid, l4, 0, 6, GaConfig(population_size=96, generations=2,
+                                       translation_bounds=(spec.origin, spec.upper)),
+             0, 0, _abi.MODE_FAST, 7 + int(b4.n_torsions.max()))
+    for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
+        out[f"team_ga_{k}"] = v
     mg = gridmaps.load_grid_set(fx.GOLDEN / "ref_grid_odd.mugd")
     out["mugd_odd"] = mg.device_grid.download()
     flags = ctypes.c_uint32(0)
