@@ -853,8 +853,10 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             const int per_sm = std::max(1, vd::ga_occupancy(false, L.npp, L.tpp, L.lay.base.bytes, gv.yz != nullptr));
             const int slots = per_sm * sms;
+            /* the whole call's ligands count: the buckets run concurrently, so a small bucket
+               of a large batch (cfg2's <= 24-atom tail) must not split (-3% when it did) */
             int team = 1;
-            while (team < 8 && (double)v.size() * team / slots < 6.0 && v.size() * team < (size_t)(8 * slots)) team *= 2;
+            while (team < 8 && (double)count * team / slots < 6.0 && (size_t)count * team < (size_t)(8 * slots)) team *= 2;
             if (const char *ov = getenv("VD_GA_TEAM")) team = std::max(1, std::min(8, atoi(ov)));
             L.lay.team = team;
             if (team > 1) L.lay.r3 = 0;  /* the team kernel has no 3-CTA register variant */
