@@ -41,10 +41,16 @@ thread_local int64_t g_launches = 0;
 
 void set_error(const std::string &msg) { g_err = msg; }
 
+static thread_local std::string g_detail;  /* why a launch helper refused (set_detail) */
+
+void set_detail(const std::string &msg) { g_detail = msg; }
+
 bool check(cudaError_t e, const char *what)
 {
     if (e == cudaSuccess) return true;
     g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    if (!g_detail.empty()) g_err += " (" + g_detail + ")";
+    g_detail.clear();
     cudaGetLastError();
     return false;
 }

@@ -46,6 +46,7 @@ struct vd_ligands {
 namespace vdi {
 void set_error(const std::string &msg);
 bool check(cudaError_t e, const char *what);
+void set_detail(const std::string &msg);  /* reason attached to the next failed check() */
 bool is_device_ptr(const void *p);
 extern thread_local int64_t g_launches;
 vd::GridView grid_view(const vd_grid *g, int elec_map, int desolv_map);

@@ -166,8 +166,10 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
                 return 0;
             }
         }
-    vdi::set_error("ligand too large for the shared-memory pose tile (n_atoms = " +
-                   std::to_string(n_atoms) + ")");
+    const std::string why = "ligand too large for the shared-memory pose tile (n_atoms = " +
+                            std::to_string(n_atoms) + ")";
+    vdi::set_error(why);
+    vdi::set_detail(why);
     return -1;
 }
 
