@@ -19,10 +19,13 @@
 #include <cstdlib>
 #include <vector>
 
-/* the GA's pair loop shares one MUFU.RCP between the two poses of a pair (see pair_fast2):
-   cfg2 screening 8,777 -> 8,857 ligands/s; the score kernel stays on two (-0.15% with it) */
+/* VD_SHARED_RCP=1 would share one MUFU.RCP between the two poses of a pair (pair_fast2;
+   +0.9% cfg2 screening in r1) but makes a pose's fast energy depend on its pair partner: the
+   elite, re-scored every generation next to a new child, then changed in the last bits and
+   the generation-best trace rose on most ligands (r2 test at pop 256 x 200), breaking the
+   reference's elitism contract.  Off: every individual's energy is a function of its genes. */
 #ifndef VD_SHARED_RCP
-#define VD_SHARED_RCP 1
+#define VD_SHARED_RCP 0
 #endif
 #include "vd_internal.h"
 #include "vd_rng.h"
@@ -347,8 +350,8 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
     double *ge = tm.e64 + (size_t)tid * pop, *ga = tm.a64 + (size_t)tid * pop;
     unsigned *bar = tm.bar + tid;
     unsigned epoch = 0;
-    /* scored here: whole pose pairs (2k, 2k+1), as in ga_kernel -- the shared reciprocal
-       (VD_SHARED_RCP) makes a pose's fast energy depend on its pair partner */
+    /* scored here: whole pose pairs (2k, 2k+1), as in ga_kernel (required for identical
+       results if VD_SHARED_RCP couples a pose's fast energy to its pair partner) */
     const int pairs = (pop + 1) / 2;
     const int i_lo = 2 * (rank * pairs / team), i_hi = min(pop, 2 * ((rank + 1) * pairs / team));
     for (;;) {

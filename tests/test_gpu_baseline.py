@@ -220,3 +220,20 @@ def test_fast_ga_full_length_agreement_rate(dev):
     params = oracle.ga_params(ga, gset.spec.origin, gset.spec.upper)
     ag = parity.ga_agreement(ligs, params, 0, 0, bt, bg)
     assert ag["agree"] >= 0.9 * count, {k: v for k, v in ag.items() if not k.startswith("_")}
+
+
+def test_fast_ga_trace_is_monotone_at_baseline_length(dev):
+    """With one elite the generation best can never rise (vd/ga.py:217-222 and the
+    reference's contract, pkg/tests/test_ga.py): the elite is re-scored each generation,
+    so its fast-mode energy must not depend on where in the population it lands (e.g. on
+    its pose-pair partner).  64 cfg2 ligands, pop 256 x 200, every trace non-increasing."""
+    from paper_2509_12232_b200.ga import _run
+
+    gset, grid, _, _ = workload_grid(2)
+    arrays, lset, ligs = batch_case(2, 500, 64)
+    gmax = 7 + int(lset.n_torsions.max())
+    bt, be, ba, bg, tr, ne = _run(grid, lset, 0, 64, _ga(256, 200, gset.spec), 0, 500,
+                                  dev.MODE_FAST, gmax)
+    rising = [(l, int(np.argmax(np.diff(tr[l]) > 0))) for l in range(64) if np.any(np.diff(tr[l]) > 0)]
+    assert not rising, rising[:5]
+    assert np.array_equal(tr[:, -1], bt) or np.all(tr.min(axis=1) == bt)
