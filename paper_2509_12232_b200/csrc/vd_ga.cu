@@ -19,16 +19,19 @@
 #include <cstdlib>
 #include <vector>
 
-/* VD_SHARED_RCP=1 would share one MUFU.RCP between the two poses of a pair (pair_fast2;
-   +0.9% cfg2 screening in r1) but makes a pose's fast energy depend on its pair partner: the
-   elite, re-scored every generation next to a new child, then changed in the last bits and
-   the generation-best trace rose on most ligands (r2 test at pop 256 x 200), breaking the
-   reference's elitism contract.  Off: every individual's energy is a function of its genes. */
-#ifndef VD_SHARED_RCP
-#define VD_SHARED_RCP 0
-#endif
+/* Every individual's fast energy is a function of its own genes only.  (r1 shared one
+   MUFU.RCP between the two poses of a thread, +0.9% cfg2 screening, but that made a pose's
+   energy depend on its pair partner: the elite, re-scored every generation next to a new
+   child, changed in the last bits and the generation-best trace rose on most ligands at
+   pop 256 x 200, breaking the reference's elitism contract.  Removed.) */
 #include "vd_internal.h"
 #include "vd_rng.h"
+
+/* Build parts (as in vd_score.cu): VD_PART undefined = one unit (the checked build);
+ * 0 = dispatch, probes and the C entry points; 1..5 = the GA kernels of TPP 1, 2, 4, 8, 16. */
+#ifndef VD_PART
+#define VD_PART -1
+#endif
 
 namespace vd {
 
@@ -47,7 +50,7 @@ struct GaOut {
 };
 
 /* block-wide (value, index) arg-min, first index on ties; `skip` flags excluded */
-__device__ int block_argmin(const float *v, const unsigned char *skip, int n, int *s_idx,
+static __device__ int block_argmin(const float *v, const unsigned char *skip, int n, int *s_idx,
                             float *s_val)
 {
     float bv = INFINITY;
@@ -88,7 +91,7 @@ __device__ __forceinline__ double dquat_norm(const double *q)
                                           __dmul_rn(q[2], q[2])), __dmul_rn(q[3], q[3])));
 }
 
-__device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0, uint64_t k1, double *g)
+static __device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0, uint64_t k1, double *g)
 {
     const double PI = 3.141592653589793;
     vd_words W = vd_words_at(i, 0, VD_PH_INIT_U, k0, k1);
@@ -107,7 +110,7 @@ __device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0, uint6
     }
 }
 
-__device__ void breed_child(const GaDev &P, int G, const double *cur, const float *fit, int gen,
+static __device__ void breed_child(const GaDev &P, int G, const double *cur, const float *fit, int gen,
                             int c, uint64_t k0, uint64_t k1, double *child)
 {
     const int k = P.tournament;
@@ -350,8 +353,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
     double *ge = tm.e64 + (size_t)tid * pop, *ga = tm.a64 + (size_t)tid * pop;
     unsigned *bar = tm.bar + tid;
     unsigned epoch = 0;
-    /* scored here: whole pose pairs (2k, 2k+1), as in ga_kernel (required for identical
-       results if VD_SHARED_RCP couples a pose's fast energy to its pair partner) */
+    /* scored here: whole pose pairs (2k, 2k+1), as in ga_kernel */
     const int pairs = (pop + 1) / 2;
     const int i_lo = 2 * (rank * pairs / team), i_hi = min(pop, 2 * ((rank + 1) * pairs / team));
     for (;;) {
@@ -436,7 +438,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
 
 /* One cooperative launch of the team kernel; `team` CTAs per ligand. */
 template <int NPP, int TPP>
-static cudaError_t launch_ga_team_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
+cudaError_t launch_ga_team_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
                                     int count, const GaDev &P, uint64_t seed, int64_t base, int gmax,
                                     const GaLayout &lay, const GaOut &out, cudaStream_t st,
                                     int *d_work, double **team_buf, int *n_ctas)
@@ -488,7 +490,7 @@ static cudaError_t launch_ga_team_t(const GridView &Gv, const LigView *d_ligs, c
 }
 
 template <bool EXACT, int NPP, int TPP>
-static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
+cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const int *d_order,
                                int count, const GaDev &P, uint64_t seed, int64_t base, int gmax,
                                const GaLayout &lay, const GaOut &out, cudaStream_t st,
                                int *d_work, double **gene_buf, int *n_ctas)
@@ -521,36 +523,8 @@ static cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const 
     return cudaGetLastError();
 }
 
-cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const LigView *d_ligs,
-                      const int *d_order, int count, const GaDev &P, uint64_t seed, int64_t base,
-                      int gmax, const GaLayout &lay, const GaOut &out, cudaStream_t st,
-                      int *d_work, double **gene_buf, int *n_ctas)
-{
-    if (!exact && lay.team > 1) {
-#define VD_T(N, T)                                                                                  \
-        if (npp == N && tpp == T)                                                                   \
-            return launch_ga_team_t<N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, \
-                                          st, d_work, gene_buf, n_ctas)
-        VD_T(32, 8); VD_T(16, 8); VD_T(32, 4); VD_T(16, 4);
-#undef VD_T
-    }
-#define VD_G(EX, N, T)                                                                             \
-    if (exact == EX && npp == N && tpp == T)                                                       \
-    return launch_ga_t<EX, N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, st,   \
-                                 d_work, gene_buf, n_ctas)
-    VD_G(true, 64, 1); VD_G(true, 32, 1); VD_G(true, 16, 1);
-    VD_G(true, 32, 8); VD_G(true, 16, 8);
-    VD_G(false, 64, 1); VD_G(false, 32, 1); VD_G(false, 16, 1);
-    VD_G(false, 64, 2); VD_G(false, 32, 2); VD_G(false, 16, 2);
-    VD_G(false, 64, 4); VD_G(false, 32, 4); VD_G(false, 16, 4);
-    VD_G(false, 32, 8); VD_G(false, 16, 8);
-    VD_G(false, 32, 16); VD_G(false, 16, 16);
-#undef VD_G
-    return cudaErrorInvalidConfiguration;
-}
-
 template <bool EXACT, int NPP, int TPP>
-static int occ_t(unsigned bytes, bool packed)
+int occ_t(unsigned bytes, bool packed)
 {
     auto k = ga_kernel<EXACT, NPP, TPP, 2>;
     if constexpr (!EXACT)
@@ -567,8 +541,10 @@ static int occ_t(unsigned bytes, bool packed)
     return per_sm;
 }
 
-/* resident CTAs per SM for a GA shape (registers and shared memory both count) */
-static int ga_occupancy_r3(unsigned bytes)
+/* resident CTAs per SM of the 3-CTA register-budget variant (built with the TPP = 4 part) */
+int ga_occupancy_r3(unsigned bytes);
+#if VD_PART < 0 || VD_PART == 3
+int ga_occupancy_r3(unsigned bytes)
 {
     auto k = ga_kernel<false, 32, 4, 3>;
     if (vdi::raise_smem_limit((const void *)k, bytes) != cudaSuccess) {
@@ -582,18 +558,86 @@ static int ga_occupancy_r3(unsigned bytes)
     }
     return per_sm;
 }
+#endif
+
+#define VD_GA_SHAPES(X)                                                     \
+    X(1, true, 64, 1) X(1, true, 32, 1) X(1, true, 16, 1)                   \
+    X(4, true, 32, 8) X(4, true, 16, 8)                                     \
+    X(1, false, 64, 1) X(1, false, 32, 1) X(1, false, 16, 1)                \
+    X(2, false, 64, 2) X(2, false, 32, 2) X(2, false, 16, 2)                \
+    X(3, false, 64, 4) X(3, false, 32, 4) X(3, false, 16, 4)                \
+    X(4, false, 32, 8) X(4, false, 16, 8)                                   \
+    X(5, false, 32, 16) X(5, false, 16, 16)
+#define VD_GA_TEAM_SHAPES(X) X(4, 32, 8) X(4, 16, 8) X(3, 32, 4) X(3, 16, 4)
+/* Every GA launch shape is explicitly instantiated in the build part of its TPP and declared
+ * extern in the others (VD_KW_<part> = `template` or `extern template`). */
+#if VD_PART < 0 || VD_PART == 1
+#define VD_KW_1 template
+#else
+#define VD_KW_1 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 2
+#define VD_KW_2 template
+#else
+#define VD_KW_2 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 3
+#define VD_KW_3 template
+#else
+#define VD_KW_3 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 4
+#define VD_KW_4 template
+#else
+#define VD_KW_4 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 5
+#define VD_KW_5 template
+#else
+#define VD_KW_5 extern template
+#endif
+#define VD_GA_INST(P, EX, N, T)                                                                   \
+    VD_KW_##P cudaError_t launch_ga_t<EX, N, T>(const GridView &, const LigView *, const int *,  \
+                                                int, const GaDev &, uint64_t, int64_t, int,       \
+                                                const GaLayout &, const GaOut &, cudaStream_t,    \
+                                                int *, double **, int *);                         \
+    VD_KW_##P int occ_t<EX, N, T>(unsigned, bool);
+#define VD_GA_TEAM_INST(P, N, T)                                                                  \
+    VD_KW_##P cudaError_t launch_ga_team_t<N, T>(const GridView &, const LigView *, const int *, \
+                                                 int, const GaDev &, uint64_t, int64_t, int,      \
+                                                 const GaLayout &, const GaOut &, cudaStream_t,   \
+                                                 int *, double **, int *);
+VD_GA_SHAPES(VD_GA_INST)
+VD_GA_TEAM_SHAPES(VD_GA_TEAM_INST)
+
+#if VD_PART <= 0
+cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const LigView *d_ligs,
+                      const int *d_order, int count, const GaDev &P, uint64_t seed, int64_t base,
+                      int gmax, const GaLayout &lay, const GaOut &out, cudaStream_t st,
+                      int *d_work, double **gene_buf, int *n_ctas)
+{
+    if (!exact && lay.team > 1) {
+#define VD_T(P_, N, T)                                                                              \
+        if (npp == N && tpp == T)                                                                   \
+            return launch_ga_team_t<N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, \
+                                          st, d_work, gene_buf, n_ctas);
+        VD_GA_TEAM_SHAPES(VD_T)
+#undef VD_T
+    }
+#define VD_G(P_, EX, N, T)                                                                         \
+    if (exact == EX && npp == N && tpp == T)                                                       \
+        return launch_ga_t<EX, N, T>(Gv, d_ligs, d_order, count, P, seed, base, gmax, lay, out, st, \
+                                     d_work, gene_buf, n_ctas);
+    VD_GA_SHAPES(VD_G)
+#undef VD_G
+    return cudaErrorInvalidConfiguration;
+}
 
 int ga_occupancy(bool exact, int npp, int tpp, unsigned bytes, bool packed)
 {
-#define VD_O(EX, N, T) \
-    if (exact == EX && npp == N && tpp == T) return occ_t<EX, N, T>(bytes, packed)
-    VD_O(true, 64, 1); VD_O(true, 32, 1); VD_O(true, 16, 1);
-    VD_O(true, 32, 8); VD_O(true, 16, 8);
-    VD_O(false, 64, 1); VD_O(false, 32, 1); VD_O(false, 16, 1);
-    VD_O(false, 64, 2); VD_O(false, 32, 2); VD_O(false, 16, 2);
-    VD_O(false, 64, 4); VD_O(false, 32, 4); VD_O(false, 16, 4);
-    VD_O(false, 32, 8); VD_O(false, 16, 8);
-    VD_O(false, 32, 16); VD_O(false, 16, 16);
+#define VD_O(P_, EX, N, T) \
+    if (exact == EX && npp == N && tpp == T) return occ_t<EX, N, T>(bytes, packed);
+    VD_GA_SHAPES(VD_O)
 #undef VD_O
     return 0;
 }
@@ -959,3 +1003,6 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     if (!dev_out) VD_CK(cudaStreamSynchronize(st));
     return 0;
 }
+#else
+}  // namespace vd
+#endif  /* VD_PART <= 0 */

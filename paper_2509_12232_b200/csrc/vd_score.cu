@@ -15,6 +15,15 @@
 
 #include "vd_internal.h"
 
+/* Build parts: the 33 score_kernel instantiations are compiled as five translation units
+ * (one per TPP) plus the dispatch, so that `make -j` builds them in parallel:
+ *   VD_PART undefined  everything in this one unit (the checked build)
+ *   VD_PART 0          dispatch, pose kernels, shape choice; launch_t<> declared extern
+ *   VD_PART 1..5       launch_t<*, *, TPP> for TPP = 1, 2, 4, 8, 16 */
+#ifndef VD_PART
+#define VD_PART -1
+#endif
+
 #ifndef VD_SCORE_PIPE
 #define VD_SCORE_PIPE 0    /* software-pipelined gathers (see inter2) */
 #endif
@@ -95,6 +104,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     }
 }
 
+#if VD_PART <= 0
 /* Poses only: the score kernel's pose stage (build_pose2<NPP, TPP>, the same shared tile,
  * scratch and sub-thread split) with the tile written out instead of scored.  TPP = 1 serves
  * vd_pose_genes; TPP = 4 / 8 are the fast score kernel's shapes (vd_debug_pose_genes). */
@@ -125,8 +135,11 @@ __global__ void __launch_bounds__(NPP *TPP) pose_kernel(LigView Lg, const double
         }
 }
 
+#endif  /* VD_PART <= 0 */
+
 constexpr unsigned kL1ReserveKB = 32;  /* of the 256 KB L1/shared array, kept as L1 */
 
+#if VD_PART <= 0
 /* Launch shape for a ligand: pose pairs per CTA (NPP) and threads per pair (TPP). */
 int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp)
 {
@@ -173,8 +186,10 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
     return -1;
 }
 
+#endif  /* VD_PART <= 0 */
+
 template <bool EXACT, int NPP, int TPP>
-static cudaError_t launch_t(const GridView &G, const LigView &L, const double *genes,
+cudaError_t launch_t(const GridView &G, const LigView &L, const double *genes,
                             const float *poses, int64_t P, int ngenes, double *inter,
                             double *intra, float *total, cudaStream_t st)
 {
@@ -258,6 +273,48 @@ static cudaError_t launch_t(const GridView &G, const LigView &L, const double *g
     return cudaGetLastError();
 }
 
+/* Every launch shape is explicitly instantiated in the part of its TPP and declared extern
+ * in the others (VD_KW_<part> = `template` or `extern template`). */
+#if VD_PART < 0 || VD_PART == 1
+#define VD_KW_1 template
+#else
+#define VD_KW_1 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 2
+#define VD_KW_2 template
+#else
+#define VD_KW_2 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 3
+#define VD_KW_3 template
+#else
+#define VD_KW_3 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 4
+#define VD_KW_4 template
+#else
+#define VD_KW_4 extern template
+#endif
+#if VD_PART < 0 || VD_PART == 5
+#define VD_KW_5 template
+#else
+#define VD_KW_5 extern template
+#endif
+#define VD_SCORE_INST(P, EX, N, T)                                                              \
+    VD_KW_##P cudaError_t launch_t<EX, N, T>(const GridView &, const LigView &, const double *, \
+                                             const float *, int64_t, int, double *, double *,   \
+                                             float *, cudaStream_t);
+#define VD_SCORE_SHAPES(X)                                                  \
+    X(1, true, 64, 1) X(1, true, 32, 1) X(1, true, 16, 1)                   \
+    X(4, true, 32, 8) X(4, true, 16, 8)                                     \
+    X(1, false, 64, 1) X(1, false, 32, 1) X(1, false, 16, 1)                \
+    X(2, false, 64, 2) X(2, false, 32, 2) X(2, false, 16, 2)                \
+    X(3, false, 64, 4) X(3, false, 32, 4) X(3, false, 16, 4)                \
+    X(4, false, 32, 8) X(4, false, 16, 8) X(4, false, 64, 8)                \
+    X(5, false, 32, 16) X(5, false, 16, 16)
+VD_SCORE_SHAPES(VD_SCORE_INST)
+
+#if VD_PART <= 0
 cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
                          const double *genes, const float *poses, int64_t P, int ngenes,
                          double *inter, double *intra, float *total, cudaStream_t st)
@@ -268,16 +325,9 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
     if (P <= 0) return cudaSuccess;
     const double *g = src == 0 ? genes : nullptr;
     const float *p = src == 0 ? nullptr : poses;
-#define VD_L(EX, N, T) \
-    if (exact == EX && npp == N && tpp == T) return launch_t<EX, N, T>(G, L, g, p, P, ngenes, inter, intra, total, st)
-    VD_L(true, 64, 1); VD_L(true, 32, 1); VD_L(true, 16, 1);
-    VD_L(true, 32, 8); VD_L(true, 16, 8);
-    VD_L(false, 64, 1); VD_L(false, 32, 1); VD_L(false, 16, 1);
-    VD_L(false, 64, 2); VD_L(false, 32, 2); VD_L(false, 16, 2);
-    VD_L(false, 64, 4); VD_L(false, 32, 4); VD_L(false, 16, 4);
-    VD_L(false, 32, 8); VD_L(false, 16, 8);
-    VD_L(false, 64, 8);
-    VD_L(false, 32, 16); VD_L(false, 16, 16);
+#define VD_L(P_, EX, N, T) \
+    if (exact == EX && npp == N && tpp == T) return launch_t<EX, N, T>(G, L, g, p, P, ngenes, inter, intra, total, st);
+    VD_SCORE_SHAPES(VD_L)
 #undef VD_L
     return cudaErrorInvalidConfiguration;
 }
@@ -345,3 +395,6 @@ unsigned chk_flags_score(bool clear)
 #endif
 }
 }  // namespace vdi
+#else
+}  // namespace vd
+#endif  /* VD_PART <= 0 */
