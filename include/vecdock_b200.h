@@ -209,7 +209,7 @@ int vd_debug_ga_init(const vd_ga_params *p, int n_torsions, uint64_t seed, uint6
 int vd_debug_ga_breed(const vd_ga_params *p, int n_torsions, const double *cur,
                       const float *fitness, int gen, uint64_t seed, uint64_t lig_index,
                       double *children);
-/* the fast score kernel's pose stage (pose tile of TPP = 4 or 8 sub-threads per pose pair,
+/* the fast score kernel's pose stage (pose tile of TPP = 4, 8 or 16 sub-threads per pose pair,
  * shared scratch, barrier-ordered torsion chain) written out as (P, 3, N) f32 poses */
 int vd_debug_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, int tpp,
                         float *poses);

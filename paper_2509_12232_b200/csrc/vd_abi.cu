@@ -733,8 +733,8 @@ int vd_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, 
 int vd_debug_pose_genes(const vd_ligands *s, int lig, const double *genes, int64_t P, int tpp,
                         float *poses)
 {
-    if (tpp != 4 && tpp != 8) {
-        set_error("vd_debug_pose_genes: tpp must be 4 or 8");
+    if (tpp != 4 && tpp != 8 && tpp != 16) {
+        set_error("vd_debug_pose_genes: tpp must be 4, 8 or 16");
         return -1;
     }
     return pose_common(s, lig, genes, P, poses, nullptr, tpp);

@@ -568,7 +568,7 @@ int ga_occupancy_r3(unsigned bytes)
     X(3, false, 64, 4) X(3, false, 32, 4) X(3, false, 16, 4)                \
     X(4, false, 32, 8) X(4, false, 16, 8)                                   \
     X(5, false, 32, 16) X(5, false, 16, 16)
-#define VD_GA_TEAM_SHAPES(X) X(4, 32, 8) X(4, 16, 8) X(3, 32, 4) X(3, 16, 4)
+#define VD_GA_TEAM_SHAPES(X) X(4, 32, 8) X(4, 16, 8) X(3, 32, 4) X(3, 16, 4) X(5, 32, 16) X(5, 16, 16)
 /* Every GA launch shape is explicitly instantiated in the build part of its TPP and declared
  * extern in the others (VD_KW_<part> = `template` or `extern template`). */
 #if VD_PART < 0 || VD_PART == 1
@@ -894,7 +894,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
            are bit-identical).
            VD_GA_TEAM=n forces a team size (1 = never split). */
         L.lay.team = 1;
-        if (!exact && (L.tpp == 8 || L.tpp == 4) && (L.npp == 32 || L.npp == 16)) {
+        if (!exact && (L.tpp == 16 || L.tpp == 8 || L.tpp == 4) && (L.npp == 32 || L.npp == 16)) {
             int dev = 0, sms = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
 #if VD_PART <= 0
 /* Poses only: the score kernel's pose stage (build_pose2<NPP, TPP>, the same shared tile,
  * scratch and sub-thread split) with the tile written out instead of scored.  TPP = 1 serves
- * vd_pose_genes; TPP = 4 / 8 are the fast score kernel's shapes (vd_debug_pose_genes). */
+ * vd_pose_genes; TPP = 4 / 8 / 16 are the fast score kernel's shapes (vd_debug_pose_genes). */
 template <int NPP, int TPP>
 __global__ void __launch_bounds__(NPP *TPP) pose_kernel(LigView Lg, const double *__restrict__ genes,
                                                         int64_t P, int ngenes, SmemLayout lay,
@@ -148,7 +148,10 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
        shared memory per pose leave few poses (and warps) per SM */
     /* EXACT: 8 subs = the reference's 8 summation lanes (intra_exact_lanes); VD_EXACT_TPP=1
        keeps one thread per pose pair (A/B, and the bitwise cross-check of both paths) */
-    int t = exact ? 8 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 4 : 8));
+    /* fast, > 96 atoms: 16 subs (512-thread CTAs at 128 registers, 16 warps per SM where the
+       pose tile leaves one CTA per SM): cfg4 GA 336 -> 365 ligands/s, scoring 52.8 -> 54.6 M
+       poses/s against 8 subs */
+    int t = exact ? 8 : (n_atoms <= 16 ? 1 : (n_atoms <= 96 ? 4 : 16));
     if (exact)
         if (const char *ov = getenv("VD_EXACT_TPP")) t = atoi(ov) == 1 ? 1 : 8;
     if (!exact)
@@ -172,6 +175,7 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
         for (int n : {64, 32, 16}) {
             if (force_npp && n != force_npp) continue;
             if (exact && t == 8 && n == 64) continue;  /* 512 threads: beyond the exact kernels' registers */
+            if (t == 16 && n == 64) continue;          /* 1,024 threads: not built */
             const unsigned b = smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes;
             if (b <= (pass == 0 && !exact ? two_ctas : limit)) {
                 *npp = n;
@@ -341,6 +345,7 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
     if (tpp_force > 0) {
         if (pick_shape(L.n_atoms, L.n_pairs, L.n_torsions, false, &npp, &tpp)) return cudaErrorInvalidValue;
         tpp = tpp_force;
+        if (tpp == 16 && npp == 64) npp = 32;  /* 64 x 16 is not built */
         const unsigned b = smem_layout(L.n_atoms, L.n_torsions, L.n_frag, npp, tpp, 0, 0).bytes;
         if (b > 200u * 1024u) return cudaErrorInvalidValue;
     } else if (pick_shape(L.n_atoms, 0, L.n_torsions, true, &npp, &tpp)) {
@@ -361,6 +366,7 @@ cudaError_t launch_pose(const LigView &L, const double *genes, int64_t P, int ng
     VD_P(64, 1) else VD_P(32, 1) else VD_P(16, 1)
     else VD_P(64, 4) else VD_P(32, 4) else VD_P(16, 4)
     else VD_P(64, 8) else VD_P(32, 8) else VD_P(16, 8)
+    else VD_P(32, 16) else VD_P(16, 16)
 #undef VD_P
     if (e != cudaSuccess) return e;
     ++vdi::g_launches;

@@ -6,7 +6,7 @@ configs' ligand distributions, and the GA at the configs' population sizes.
   oracle on the same maps, in both modes, on the gather layout each grid gets
   (cfg0/cfg2 yz-bricks, cfg1 z-pairs, cfg4 plain): vd/scoring/simd.py:157-240,
   pkg/tests/test_scoring.py:250-267;
-* the fast score kernel's TPP = 4 / 8 pose stage, bit for bit (vd/pose.py:137-205);
+* the fast score kernel's TPP = 4 / 8 / 16 pose stage, bit for bit (vd/pose.py:137-205);
 * generation 0 of the fast GA kernel (its own scoring path: shared reciprocal,
   pipelined gathers) on 512 cfg2 and 32 cfg4 ligands vs the oracle GA with the
   same keys, and every returned best genotype re-scored by the oracle
@@ -110,9 +110,9 @@ def test_batch_configs_16k_poses(dev, cfg, count, per, mode):
 
 
 @pytest.mark.parametrize("cfg,count", [(1, 1), (2, 6), (4, 2)])
-@pytest.mark.parametrize("tpp", [4, 8])
+@pytest.mark.parametrize("tpp", [4, 8, 16])
 def test_score_kernel_pose_stage_bitwise(dev, cfg, count, tpp):
-    """The TPP = 4/8 pose path every fast launch uses (spread sincos, sub-shared
+    """The TPP = 4/8/16 pose path every fast launch uses (spread sincos, sub-shared
     matrices, barrier-ordered torsion chain, packed fma(x, one, y)) vs the oracle's
     reference-sequence poses, bit for bit."""
     from paper_2509_12232_b200 import synth

@@ -270,7 +270,7 @@ def test_fast_mode_every_grid_layout(cuda, name, layout, monkeypatch):
     assert np.array_equal(e.view(np.uint64), e0.view(np.uint64))
 
 
-@pytest.mark.parametrize("tpp", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("tpp", ["1", "2", "4", "8", "16"])
 def test_fast_mode_every_launch_shape(cuda, tpp, monkeypatch):
     """Every threads-per-pose-pair shape gives the same poses and in-tolerance energies."""
     from paper_2509_12232_b200.backend import CudaBackend

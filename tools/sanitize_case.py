@@ -1,10 +1,10 @@
 """Small invocations of every hot kernel shape, with all outputs saved, for the checked-
 build comparison (tests/test_gpu_checked.py; compute-sanitizer is closed on this pool).
 
-  score_kernel  TPP 4 role split (cfg1 fixture, 40 atoms, resident pairs), TPP 8 with
-                streamed pair tiles (128-atom fixture), TPP 1 exact; yz-brick, z-pair
+  score_kernel  TPP 4 role split (cfg1 fixture, 40 atoms, resident pairs), TPP 16 and 8
+                with streamed pair tiles (128-atom fixture), TPP 8 exact; yz-brick, z-pair
                 and plain grid layouts; the host-buffer pipeline path
-  pose_kernel   TPP 1 / 4 / 8
+  pose_kernel   TPP 1 / 4 / 8 / 16
   ga_kernel     fast packed, fast plain, exact, several buckets at once (incl. the
                 3-CTA r3 variant for <= 32-atom buckets); ga_team_kernel (6 cfg4
                 ligands: one ligand over 8 CTAs)
@@ -49,7 +49,13 @@ def main(out_path):
                 for k, v in zip("eat", b.score_population_arrays(c["genes"][:n], ctx)):
                     out[f"{layout}_{name}_{mode}_score_{k}"] = v
             _, ligs = CudaBackend(mode="fast", device=0).prepared(ctx)
-            for tpp in (4, 8):
+            if name == "big":  # > 96 atoms launch with 16 subs: keep the 8-sub shape covered
+                os.environ["VD_TPP"] = "8"
+                for k, v in zip("eat", CudaBackend(mode="fast", device=0).score_population_arrays(
+                        c["genes"][:n], ctx)):
+                    out[f"{layout}_{name}_fast_score8_{k}"] = v
+                del os.environ["VD_TPP"]
+            for tpp in (4, 8, 16):
                 out[f"{layout}_{name}_pose{tpp}"] = _abi.debug_pose_genes(ligs, 0, c["genes"][:n], tpp)
             out[f"{layout}_{name}_pose1"] = CudaBackend(mode="fast", device=0).pose_population(
                 c["genes"][:n], ctx)
