@@ -496,7 +496,7 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
     }
     /* fast order: stable partition by the 12-10 flag (one hb-uniform stream each) */
     std::vector<float4> fcoef(std::max(NP, 1));
-    std::vector<int> fij(std::max(NP, 1));
+    std::vector<int2> fij(std::max(NP, 1));  /* 3*i, 3*j (PairTile::off) */
     for (int l = 0; l < L; ++l) {
         const int p0 = a->pair_start[l], p1 = a->pair_start[l + 1];
         int w = p0;
@@ -505,7 +505,7 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
             for (int k = p0; k < p1; ++k)
                 if ((a->pair_hb[k] ? 1 : 0) == g) {
                     fcoef[w] = pcoef[k];
-                    fij[w] = a->pair_i[k] | (a->pair_j[k] << 16);
+                    fij[w] = make_int2(3 * a->pair_i[k], 3 * a->pair_j[k]);
                     ++w;
                 }
         }
@@ -523,9 +523,9 @@ int vd_ligands_create(const vd_ligand_arrays *a, vd_ligands **out)
               vdi::check(cudaMemcpy(s->d_tors, tors.data(), tors.size() * sizeof(int4), cudaMemcpyHostToDevice), "up tors") &&
               vdi::check(cudaMemcpy(s->d_frag, frag.data(), frag.size() * sizeof(int), cudaMemcpyHostToDevice), "up frag") &&
               vdi::check(cudaMalloc(&s->d_fcoef, fcoef.size() * sizeof(float4)), "alloc fcoef") &&
-              vdi::check(cudaMalloc(&s->d_fij, fij.size() * sizeof(int)), "alloc fij") &&
+              vdi::check(cudaMalloc(&s->d_fij, fij.size() * sizeof(int2)), "alloc fij") &&
               vdi::check(cudaMemcpy(s->d_fcoef, fcoef.data(), fcoef.size() * sizeof(float4), cudaMemcpyHostToDevice), "up fcoef") &&
-              vdi::check(cudaMemcpy(s->d_fij, fij.data(), fij.size() * sizeof(int), cudaMemcpyHostToDevice), "up fij");
+              vdi::check(cudaMemcpy(s->d_fij, fij.data(), fij.size() * sizeof(int2), cudaMemcpyHostToDevice), "up fij");
     if (!ok) {
         vd_ligands_destroy(s);
         return -1;

@@ -126,7 +126,7 @@ struct LigView {
     const float4 *pcoef;    /* a, b, qq, dsl (weight-folded) */
     /* fast order (FAST): 12-6 pairs, then the n_pairs - n_nohb 12-10 pairs */
     const float4 *fcoef;
-    const int *fij;         /* i | j << 16 */
+    const int2 *fij;        /* 3*i, 3*j: pose-tile offsets in units of NPP elements (PairTile::off) */
     int n_nohb;
     float tors32, cut2, penalty;
     int elec_map, desolv_map;
@@ -222,6 +222,22 @@ __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __
 __device__ __forceinline__ float mufu_rsq(float x) { float y; asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float mufu_ex2(float x) { float y; asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float mufu_rcp(float x) { float y; asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
+
+/* cp.async (LDGSTS): global -> shared without staging registers */
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+#ifdef VD_CPASYNC_CA
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem) : "memory");
+#else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem) : "memory");
+#endif
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 #define VD_S2(i, c) S[(3 * (i) + (c)) * NPP]
 
@@ -867,8 +883,8 @@ __device__ __forceinline__ float2 flat_fast(const float2 *S, int kb, int ke, con
 #pragma unroll kFlatUnroll
     for (int k = kb + sub; k < ke; k += TPP) {
         const float4 c = tc[k];
-        const int2 o = toff[k];  /* element offsets 3*NPP*i, 3*NPP*j into the pose tile */
-        const float2 *Si = S + o.x, *Sj = S + o.y;
+        const int2 o = toff[k];  /* 3*i, 3*j: pose-tile offsets in units of NPP elements */
+        const float2 *Si = S + o.x * NPP, *Sj = S + o.y * NPP;
         acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(Si[0], Sj[0]), fsub2(Si[NPP], Sj[NPP]),
                                              fsub2(Si[2 * NPP], Sj[2 * NPP]), c, cut2));
     }
@@ -906,11 +922,11 @@ __device__ __forceinline__ float2 rows_fast(const float2 *S, int kb, int ke, con
         const int2 o = toff[k];
         if (o.x != ci) {
             ci = o.x;
-            xi = S[o.x];
-            yi = S[o.x + NPP];
-            zi = S[o.x + 2 * NPP];
+            xi = S[o.x * NPP];
+            yi = S[o.x * NPP + NPP];
+            zi = S[o.x * NPP + 2 * NPP];
         }
-        const float2 *Sj = S + o.y;
+        const float2 *Sj = S + o.y * NPP;
         acc = fadd2(acc, pair_fast2<HB, CUT>(fsub2(xi, Sj[0]), fsub2(yi, Sj[NPP]),
                                              fsub2(zi, Sj[2 * NPP]), c, cut2));
     }
@@ -921,8 +937,9 @@ __device__ __forceinline__ float2 rows_fast(const float2 *S, int kb, int ke, con
 struct PairTile {
     float4 *coef;   /* [cap] weight-folded a, b, qq, dsl */
     int *j;         /* [cap] EXACT: packed ij | hb << 31 (reference order) */
-    int2 *off;      /* [cap] FAST: pose-tile element offsets 3*NPP*i, 3*NPP*j (aliases j) */
-    int cap;
+    int2 *off;      /* [cap] FAST: 3*i, 3*j -- pose-tile offsets in units of NPP elements, a raw
+                       copy of LigView::fij (aliases j) */
+    int cap;        /* pairs per buffer; a streamed FAST list has two buffers (coef + cap, off + cap) */
     bool resident;
 };
 
@@ -939,9 +956,9 @@ __device__ __forceinline__ void stage_pairs(const LigView &L, const PairTile &T,
                        (int)((__ldg(&L.pij[k0 + k]) >> 15) & 0x7fff) < L.n_atoms, VD_SITE_ATOM);
         } else {
             T.coef[k] = __ldg(&L.fcoef[k0 + k]);
-            const int w = __ldg(&L.fij[k0 + k]);
-            VD_CHK((w & 0xffff) < L.n_atoms && (w >> 16) >= 0 && (w >> 16) < L.n_atoms, VD_SITE_ATOM);
-            T.off[k] = make_int2(3 * NPP * (w & 0xffff), 3 * NPP * (w >> 16));
+            const int2 w = __ldg(&L.fij[k0 + k]);
+            VD_CHK(w.x >= 0 && w.x < 3 * L.n_atoms && w.y >= 0 && w.y < 3 * L.n_atoms, VD_SITE_ATOM);
+            T.off[k] = w;
         }
     }
 }
@@ -970,7 +987,11 @@ __device__ __forceinline__ void exact_pair(const float2 *S, const PairTile &T, i
 }
 
 /* intra of both poses over this sub's share of the pairs (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP>
+/* ASYNC (streamed FAST lists): false = one tile buffer, staged through registers (two CTA
+ * barriers per tile; the score kernel: its plain-layout gathers are sensitive to the L1 size
+ * the shared memory leaves -- a second 6 KB buffer cost cfg4 scoring 9%); true = two buffers
+ * filled by cp.async (one barrier per tile, tiles of up to 2,048 pairs; the GA kernels) */
+template <bool EXACT, int NPP, int TPP, bool ASYNC = false>
 __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const PairTile &T,
                                        int sub, double &a0, double &a1,
                                        unsigned w0 = ~0u, unsigned w1 = ~0u)
@@ -1014,12 +1035,29 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
     } else {
         const bool cut = L.cut2 < INFINITY;
         double s0 = 0.0, s1 = 0.0;
-        const int step = T.resident ? n : T.cap;
-        /* streamed lists: the next tile's coefficients are loaded into registers while the
-           current tile is computed, so the L2 latency of the staging loads stays hidden */
-        constexpr int kPre = (kTile + NPP * TPP - 1) / (NPP * TPP);
+        /* Streamed lists: tiles of T.cap pairs, double-buffered.  The records are raw copies
+           of the global arrays, so every thread copies its share of tile t+1 with cp.async
+           (no staging registers) while tile t is computed; one CTA barrier per tile makes tile
+           t visible and frees the buffer tile t-1 was read from. */
+        const int cap = T.resident ? n : T.cap;
+        auto issue = [&](int t) {
+            const int t0 = t * cap, cnt = min(cap, n - t0);
+            const float4 *gc = L.fcoef + t0;
+            const int2 *go = L.fij + t0;
+            float4 *sc = T.coef + (t & 1) * cap;
+            int2 *so = T.off + (t & 1) * cap;
+            for (int k = threadIdx.x; k < cnt; k += NPP * TPP) {
+                VD_CHK(k < T.cap, VD_SITE_TILE);
+                cp_async16(sc + k, gc + k);
+                cp_async8(so + k, go + k);
+            }
+            cp_async_commit();
+        };
+        /* register-staged single buffer (tiles of kTile pairs): the next tile's records are
+           loaded into registers while the current tile is computed */
+        constexpr int kPre = ASYNC ? 1 : (kTile + NPP * TPP - 1) / (NPP * TPP);
         float4 pc[kPre];
-        int pw[kPre];
+        int2 pw[kPre];
         auto prefetch = [&](int k0) {
 #pragma unroll
             for (int r = 0; r < kPre; ++r) {
@@ -1030,38 +1068,50 @@ __device__ __forceinline__ void intra2(const LigView &L, const float2 *S, const 
                 }
             }
         };
-        if (!T.resident) prefetch(0);
-        for (int t0 = 0; t0 < n; t0 += step) {
-            const int tcnt = min(step, n - t0);
-            if (!T.resident) {
+        if (!T.resident) {
+            if (ASYNC) issue(0);
+            else prefetch(0);
+        }
+        for (int t = 0, t0 = 0; t0 < n; ++t, t0 += cap) {
+            const int tcnt = min(cap, n - t0);
+            const float4 *tc = T.coef;
+            const int2 *to = T.off;
+            if (!T.resident && !ASYNC) {
                 __syncthreads();
 #pragma unroll
                 for (int r = 0; r < kPre; ++r) {
                     const int k = (int)threadIdx.x + r * NPP * TPP;
                     if (k < tcnt) {
-                        VD_CHK(k < T.cap && (pw[r] & 0xffff) < L.n_atoms && (pw[r] >> 16) < L.n_atoms,
-                               VD_SITE_TILE);
+                        VD_CHK(k < T.cap && pw[r].x >= 0 && pw[r].x < 3 * L.n_atoms && pw[r].y >= 0 &&
+                                   pw[r].y < 3 * L.n_atoms, VD_SITE_TILE);
                         T.coef[k] = pc[r];
-                        T.off[k] = make_int2(3 * NPP * (pw[r] & 0xffff), 3 * NPP * (pw[r] >> 16));
+                        T.off[k] = pw[r];
                     }
                 }
                 __syncthreads();
-                if (t0 + step < n) prefetch(t0 + step);
+                if (t0 + cap < n) prefetch(t0 + cap);
+            }
+            if (!T.resident && ASYNC) {
+                cp_async_wait_all();
+                __syncthreads();
+                if (t0 + cap < n) issue(t + 1);
+                tc += (t & 1) * cap;
+                to += (t & 1) * cap;
             }
             /* fp32 partials per kTile chunk, flushed to fp64 */
             for (int c0 = 0; c0 < tcnt; c0 += kTile) {
                 const int kb = c0, ke = min(tcnt, c0 + kTile);
                 const int kh = min(ke, max(kb, L.n_nohb - t0));  /* 12-6 | 12-10 boundary */
 #if VD_INTRA_ROWS
-                float2 part = cut ? rows_fast<NPP, false, true>(S, kb, kh, T.coef, T.off, w0, w1, L.cut2)
-                                  : rows_fast<NPP, false, false>(S, kb, kh, T.coef, T.off, w0, w1, L.cut2);
-                part = fadd2(part, cut ? rows_fast<NPP, true, true>(S, kh, ke, T.coef, T.off, w0, w1, L.cut2)
-                                       : rows_fast<NPP, true, false>(S, kh, ke, T.coef, T.off, w0, w1, L.cut2));
+                float2 part = cut ? rows_fast<NPP, false, true>(S, kb, kh, tc, to, w0, w1, L.cut2)
+                                  : rows_fast<NPP, false, false>(S, kb, kh, tc, to, w0, w1, L.cut2);
+                part = fadd2(part, cut ? rows_fast<NPP, true, true>(S, kh, ke, tc, to, w0, w1, L.cut2)
+                                       : rows_fast<NPP, true, false>(S, kh, ke, tc, to, w0, w1, L.cut2));
 #else
-                float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, kh, T.coef, T.off, sub, L.cut2)
-                                  : flat_fast<NPP, TPP, false, false>(S, kb, kh, T.coef, T.off, sub, L.cut2);
-                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, ke, T.coef, T.off, sub, L.cut2)
-                                       : flat_fast<NPP, TPP, true, false>(S, kh, ke, T.coef, T.off, sub, L.cut2));
+                float2 part = cut ? flat_fast<NPP, TPP, false, true>(S, kb, kh, tc, to, sub, L.cut2)
+                                  : flat_fast<NPP, TPP, false, false>(S, kb, kh, tc, to, sub, L.cut2);
+                part = fadd2(part, cut ? flat_fast<NPP, TPP, true, true>(S, kh, ke, tc, to, sub, L.cut2)
+                                       : flat_fast<NPP, TPP, true, false>(S, kh, ke, tc, to, sub, L.cut2));
 #endif
                 s0 += (double)part.x;
                 s1 += (double)part.y;
@@ -1117,7 +1167,8 @@ __device__ __forceinline__ void intra_exact_lanes(const LigView &L, const float2
 }
 
 /* inter + intra of both poses (all CTA threads must call) */
-template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0, bool FLAT = false>
+template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0, bool FLAT = false,
+          bool ASYNC = false>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
                                         double &a0, double &a1, double *red = nullptr, int pp = 0)
@@ -1163,7 +1214,7 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
         return;
     }
     inter2<EXACT, NPP, TPP, PIPE, LAY, FLAT>(L, G, S, sub, 0, L.n_atoms, e0, e1);
-    intra2<EXACT, NPP, TPP>(L, S, T, sub, a0, a1);
+    intra2<EXACT, NPP, TPP, ASYNC>(L, S, T, sub, a0, a1);
 }
 
 __device__ __forceinline__ float total32(double inter, double intra, float tors)
@@ -1207,8 +1258,12 @@ struct SmemLayout {
 __host__ __device__ inline unsigned align16(unsigned v) { return (v + 15u) & ~15u; }
 
 /* n_pairs: the largest pair list the launch serves (selects resident vs streamed). */
+/* A streamed FAST list takes stream_bufs buffers of stream_cap pairs (a multiple of kTile):
+ * 1 x kTile, register-staged (the score kernel), or 2 x up to 2,048 filled by cp.async (the
+ * GA kernels); see intra2. */
 __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n_frag, int npp,
-                                                  int tpp, unsigned extra, int n_pairs)
+                                                  int tpp, unsigned extra, int n_pairs,
+                                                  int stream_cap = kTile, int stream_bufs = 1)
 {
     SmemLayout s;
     unsigned off = align16(8u * 3u * (unsigned)n_atoms * (unsigned)npp);
@@ -1224,17 +1279,18 @@ __host__ __device__ inline SmemLayout smem_layout(int n_atoms, int n_tors, int n
     s.scratch = off;
     off = align16(off + scratch_bytes);
     s.resident = n_pairs <= kResidentPairs;
-    s.cap = s.resident ? (((n_pairs > 0 ? n_pairs : 1) + 7) & ~7) : kTile;
+    s.cap = s.resident ? (((n_pairs > 0 ? n_pairs : 1) + 7) & ~7) : stream_cap;
+    const unsigned nbuf = s.resident ? 1u : (unsigned)stream_bufs;
     s.tile_coef = off;
-    off += 16u * (unsigned)s.cap;
+    off += 16u * nbuf * (unsigned)s.cap;
     s.tile_idx = off;
-    off = align16(off + 8u * (unsigned)s.cap);
+    off = align16(off + 8u * nbuf * (unsigned)s.cap);
     /* the sub reduction reuses the pose scratch (the pose stage is over when it runs;
        the GA syncs before the next tile's pose stage) or a streamed pair tile */
     const unsigned red_bytes = (tpp > 1) ? 8u * 4u * (unsigned)tpp * (unsigned)npp : 0u;
     if (red_bytes <= scratch_bytes) {
         s.red = s.scratch;
-    } else if (!s.resident && red_bytes <= 24u * (unsigned)s.cap) {
+    } else if (!s.resident && red_bytes <= 16u * nbuf * (unsigned)s.cap) {  /* the coef buffers */
         s.red = s.tile_coef;
     } else {
         s.red = off;

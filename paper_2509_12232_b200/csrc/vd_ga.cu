@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : (LAY == 3
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, (LAY == 3 ? 1 : LAY)>(
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, (LAY == 3 ? 1 : LAY), false, true>(
                     L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
                 reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, LAY>(
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, LAY, false, true>(
                     L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
                 reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
@@ -858,7 +858,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         for (int npp : {32, 64, 16}) {  /* ties -> 32 (cfg2 A/B: 6078 vs 5837 ligands/s) */
             if (force && atoi(force) != npp) continue;
             vd::GaLayout lay;
-            lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra, pmax);
+            lay.base = vd::smem_layout(nmax, tb, fb, npp, L.tpp, extra, pmax, vd::kTile, exact ? 1 : 2);
             if (lay.base.bytes > 227u * 1024u) continue;
             if (npp * L.tpp < 32) continue;  /* block_argmin's shuffles need whole warps */
             int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes, gv.yz != nullptr) * npp * L.tpp / 32;
@@ -887,6 +887,23 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         if (best_warps <= 0) {
             set_error("vd_dock_batch: population scratch + pose tile exceed shared memory");
             return -1;
+        }
+        /* streamed pair lists (> kResidentPairs, e.g. cfg4's ~7,600): the largest double-
+           buffered tile that keeps the resident CTAs -- one CTA barrier per tile, so a 2,048-
+           pair tile means 4 barriers per pose tile for cfg4 instead of 30.  VD_STREAM_CAP
+           forces a size (a multiple of 256). */
+        if (!L.lay.base.resident && !exact) {
+            const int occ0 = vd::ga_occupancy(false, L.npp, L.tpp, L.lay.base.bytes, gv.yz != nullptr);
+            int caps[] = {2048, 1024, 512};
+            if (const char *ov = getenv("VD_STREAM_CAP")) caps[0] = caps[1] = caps[2] = std::max(256, atoi(ov) & ~255);
+            for (int cap : caps) {
+                vd::GaLayout lay = L.lay;
+                lay.base = vd::smem_layout(nmax, tb, fb, L.npp, L.tpp, extra, pmax, cap, 2);
+                if (lay.base.bytes > 227u * 1024u) continue;
+                if (vd::ga_occupancy(false, L.npp, L.tpp, lay.base.bytes, gv.yz != nullptr) < occ0) continue;
+                L.lay = lay;
+                break;
+            }
         }
         /* teams: with few ligands per CTA slot (BASELINE cfg4 at 8 GPUs: 250 ligands on 148
            one-CTA SMs, 1.7 waves; a single dock: 1 ligand) a ligand's population is split over

@@ -38,7 +38,7 @@ struct vd_ligands {
     int4 *d_tors;
     int *d_frag;
     float4 *d_fcoef;          /* fast-order pairs: 12-6 then 12-10 */
-    int *d_fij;               /* i | j << 16 */
+    int2 *d_fij;              /* 3*i, 3*j */
     std::vector<int> n_nohb, n_frag;
     vd::LigView view(int lig) const;
 };
