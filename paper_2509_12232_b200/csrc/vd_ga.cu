@@ -15,8 +15,10 @@
  * Philox4x64-10 with IEEE-exact transforms, identical to the CPU oracle's.
  */
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 #include <vector>
 
 /* Every individual's fast energy is a function of its own genes only.  (r1 shared one
@@ -166,7 +168,6 @@ static __device__ void breed_child(const GaDev &P, int G, const double *cur, con
 struct GaLayout {
     SmemLayout base;          /* pose tile + pair tiles (+ reduction) for the largest ligand */
     unsigned off_fit, off_e, off_a, off_taken;
-    int r3 = 0;               /* host: launch the 3-CTA register-budget variant (LAY 3) */
     int team = 1;             /* host: CTAs per ligand (ga_team_kernel when > 1) */
 };
 
@@ -183,7 +184,11 @@ struct GaTeam {
 #define VD_GA_MINB 1
 #endif
 #ifndef VD_GA_SPLIT
-#define VD_GA_SPLIT 0  /* role-split energy stage (see energy2; slower for the GA, measured) */
+#define VD_GA_SPLIT 1  /* role-split energy stage (see energy2), as in pop_score_kernel: both GA
+                          paths then partition a ligand's fp32 pair sums alike and give
+                          bit-identical energies (alone, the split costs the 4-warp persistent
+                          CTAs ~19%; they now serve only batches too small for the
+                          generation-synchronous path, and ligands it does not cover) */
 #endif
 #ifndef VD_GA_PIPE
 #define VD_GA_PIPE 1   /* software-pipelined grid gathers (see inter2) */
@@ -191,19 +196,21 @@ struct GaTeam {
 #ifndef VD_GA_REGS
 #define VD_GA_REGS 0   /* >0: register cap per thread (min resident CTAs derived from it) */
 #endif
+/* both GA paths split the energy stage for 4 and 8 subs (the shapes of ligands up to 96
+   atoms); the 16-sub kernels (cfg4: streamed pair lists, which never split) stay without
+   the split code, which cost them 780 B of spills */
+__host__ __device__ constexpr bool ga_split(int tpp) { return VD_GA_SPLIT != 0 && tpp <= 8; }
 constexpr int ga_minb(int threads)
 {
     return VD_GA_REGS > 0 ? (65536 / (threads * VD_GA_REGS) > 0 ? 65536 / (threads * VD_GA_REGS) : 1)
                           : VD_GA_MINB;
 }
-/* LAY: 1 packed grid, 2 plain grid, 3 packed grid with a 3-CTA register budget (168
- * registers instead of 245: for 32 x 4 tiles of small ligands, whose shared memory leaves
- * room for a third CTA that the full register budget does not) */
+/* LAY: 1 packed grid, 2 plain grid */
 #ifndef VD_GA_EXACT_MINB
 #define VD_GA_EXACT_MINB 2  /* resident CTAs the exact kernels are compiled for (cfg2 exact GA: 1 -> 2 CTAs at 128 registers, 1,017 -> 1,723 ligands/s) */
 #endif
 template <bool EXACT, int NPP, int TPP, int LAY>
-__global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : (LAY == 3 ? 3 : ga_minb(NPP *TPP))) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
+__global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : ga_minb(NPP *TPP)) ga_kernel(GridView Gv, const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, int count,
                                                       GaDev P, uint64_t seed, int64_t base,
                                                       int *work, double *gene_buf, int gmax,
@@ -255,7 +262,7 @@ __global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : (LAY == 3
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, (LAY == 3 ? 1 : LAY), false, true>(
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, ga_split(TPP), LAY, false, true>(
                     L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
                 reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
                                       reinterpret_cast<float *>(smem + lay.base.scratch) + pp, Gv.one);
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
-                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, VD_GA_SPLIT != 0, LAY, false, true>(
+                energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, ga_split(TPP), LAY, false, true>(
                     L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
                 reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
@@ -434,6 +441,110 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
         if (rank == 0 && threadIdx.x == 0) out.n_evals[l] = (int64_t)pop * (P.generations + 1);
         __syncthreads();
     }
+}
+
+/* ---- generation-synchronous GA (fast mode, batches that fill the GPU) ----------------------
+ * The persistent kernels above carry the whole GA in one CTA's registers (245 of them: 8-12
+ * warps per SM).  For a batch large enough to fill the GPU per generation, every generation
+ * is instead two launches over all the batch's ligands:
+ *   pop_score_kernel  the score kernel's stages and shape (121 registers, 2 CTAs x 256 threads,
+ *                     role-split energy stage) over (ligand, pose tile) CTAs, genes read from
+ *                     the batch's population buffer in global memory
+ *   ga_step_kernel    one CTA per ligand: generation best, elites, children (the same
+ *                     block_argmin / breed_child code and random streams as ga_kernel)
+ * Same GA, same streams; the fast energies differ from ga_kernel's in the last bits (the role
+ * split partitions the fp32 partial sums differently), each still a function of the
+ * individual's genes alone.  Populations live at pop * gmax doubles per ligand slot,
+ * individuals at stride G = 7 + T inside it (as in ga_kernel's buffers). */
+template <int NPP, int TPP, int LAY>
+__global__ void __launch_bounds__(NPP *TPP) pop_score_kernel(GridView G, const LigView *__restrict__ ligs,
+                                                             const int *__restrict__ order,
+                                                             int tiles_per_lig, int pop,
+                                                             const double *__restrict__ genes, int gmax,
+                                                             unsigned smem_bytes, float *__restrict__ fit,
+                                                             double *__restrict__ e64,
+                                                             double *__restrict__ a64)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    VD_POISON(smem, smem_bytes);
+    const int pp = threadIdx.x % NPP, sub = threadIdx.x / NPP;
+    const int slot = blockIdx.x / tiles_per_lig, tile = blockIdx.x % tiles_per_lig;
+    float2 *S = reinterpret_cast<float2 *>(smem) + pp;
+    /* the layout of THIS ligand (the launch's shared memory is the largest of its group's
+       layouts; one made of the group's maxima would be larger than any of them) */
+    const LigView &Lg = ligs[order[slot]];
+    const SmemLayout lay = smem_layout(Lg.n_atoms, Lg.n_torsions, Lg.n_frag, NPP, TPP, 0, Lg.n_pairs);
+    VD_CHK(lay.bytes <= smem_bytes, VD_SITE_SMEM);
+    const PairTile T = pair_tile(smem, lay);
+    const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2,
+                                     lay.topo_tors, lay.topo_frag);
+    stage_resident<false, NPP>(L, T);
+    __syncthreads();
+    const int Gn = 7 + L.n_torsions;
+    const int i0 = (tile * NPP + pp) * 2, i1 = i0 + 1;
+    const double *gb = genes + (size_t)slot * pop * gmax;
+    build_pose2<NPP, TPP>(L, gb + (size_t)min(i0, pop - 1) * Gn, gb + (size_t)min(i1, pop - 1) * Gn, S,
+                          sub, reinterpret_cast<float *>(smem + lay.scratch) + pp, G.one);
+    if (TPP > 1) __syncthreads();
+    double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
+    energy2<false, NPP, TPP, false, ga_split(TPP), LAY>(L, G, S, T, sub, e0, e1, a0, a1,
+                                               reinterpret_cast<double *>(smem + lay.red), pp);
+    reduce_subs<NPP, TPP, false>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
+    if (sub == 0) {
+        const size_t o = (size_t)slot * pop;
+        if (i0 < pop) { e64[o + i0] = e0; a64[o + i0] = a0; fit[o + i0] = total32(e0, a0, L.tors32); }
+        if (i1 < pop) { e64[o + i1] = e1; a64[o + i1] = a1; fit[o + i1] = total32(e1, a1, L.tors32); }
+    }
+}
+
+/* One generation's scoring launch.  setup: raise the shared-memory limit and work out the
+ * carveout (as many CTAs as fit beside a 32 KB L1 share, see vd_score.cu's launch_t) into
+ * *pct; later launches pass it back.  The carveout is a per-function attribute and size
+ * buckets share functions, so it is set under a lock right before every launch. */
+template <int NPP, int TPP>
+cudaError_t launch_pop_t(const GridView &Gv, const LigView *d_ligs, const int *d_order, int count,
+                         int pop, const double *genes, int gmax, unsigned bytes, float *fit,
+                         double *e64, double *a64, cudaStream_t st, bool setup, int *pct)
+{
+    auto k = pop_score_kernel<NPP, TPP, 2>;
+    if (Gv.yz != nullptr) k = pop_score_kernel<NPP, TPP, 1>;
+    static std::mutex mu;
+    static int last_pct[2][16];  /* [layout][device]: the carveout last set, + 1 */
+    std::lock_guard<std::mutex> lk(mu);
+    int dev_now = 0;
+    cudaGetDevice(&dev_now);
+    int &last = last_pct[Gv.yz != nullptr][dev_now & 15];
+    if (setup) {
+        last = 0;
+        cudaError_t e = vdi::raise_smem_limit((const void *)k, bytes);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
+        int occ = 0, dev = 0, smem_sm = 0, resv = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NPP * TPP, bytes);
+        if (e != cudaSuccess) return e;
+        int fit_ctas = (smem_sm - 32 * 1024) / (int)(bytes + resv);
+        if (fit_ctas < 2) fit_ctas = std::min(2, smem_sm / (int)(bytes + resv));  /* 2 CTAs beat the L1 share */
+        const int want = std::max(1, std::min(occ, fit_ctas));
+        *pct = std::min(100, (int)((100LL * want * (bytes + resv) + smem_sm - 1) / smem_sm));
+        if (getenv("VD_VERBOSE"))
+            fprintf(stderr, "[vd] pop_score_kernel<%d,%d> %d ligands smem=%u ctas/sm=%d carveout=%d%%\n",
+                    NPP, TPP, count, bytes, want, *pct);
+        return cudaSuccess;
+    }
+    if (last != *pct + 1) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, *pct);
+        if (e != cudaSuccess) return e;
+        last = *pct + 1;
+    }
+    const int tiles = (pop + 2 * NPP - 1) / (2 * NPP);
+    k<<<(unsigned)((size_t)count * tiles), NPP * TPP, bytes, st>>>(Gv, d_ligs, d_order, tiles, pop, genes,
+                                                                      gmax, bytes, fit, e64, a64);
+    ++vdi::g_launches;
+    return cudaGetLastError();
 }
 
 /* One cooperative launch of the team kernel; `team` CTAs per ligand. */
@@ -498,8 +609,6 @@ cudaError_t launch_ga_t(const GridView &Gv, const LigView *d_ligs, const int *d_
     auto k = ga_kernel<EXACT, NPP, TPP, 2>;  /* plain grid (and every exact launch) */
     if constexpr (!EXACT)
         if (Gv.yz != nullptr) k = ga_kernel<EXACT, NPP, TPP, 1>;  /* packed grid */
-    if constexpr (!EXACT && NPP == 32 && TPP == 4)
-        if (Gv.yz != nullptr && lay.r3) k = ga_kernel<EXACT, NPP, TPP, 3>;
     const unsigned bytes = lay.base.bytes;
     cudaError_t e = vdi::raise_smem_limit((const void *)k, bytes);
     if (e != cudaSuccess) return e;
@@ -541,25 +650,6 @@ int occ_t(unsigned bytes, bool packed)
     return per_sm;
 }
 
-/* resident CTAs per SM of the 3-CTA register-budget variant (built with the TPP = 4 part) */
-int ga_occupancy_r3(unsigned bytes);
-#if VD_PART < 0 || VD_PART == 3
-int ga_occupancy_r3(unsigned bytes)
-{
-    auto k = ga_kernel<false, 32, 4, 3>;
-    if (vdi::raise_smem_limit((const void *)k, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 128, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return per_sm;
-}
-#endif
-
 #define VD_GA_SHAPES(X)                                                     \
     X(1, true, 64, 1) X(1, true, 32, 1) X(1, true, 16, 1)                   \
     X(4, true, 32, 8) X(4, true, 16, 8)                                     \
@@ -569,6 +659,9 @@ int ga_occupancy_r3(unsigned bytes)
     X(4, false, 32, 8) X(4, false, 16, 8)                                   \
     X(5, false, 32, 16) X(5, false, 16, 16)
 #define VD_GA_TEAM_SHAPES(X) X(4, 32, 8) X(4, 16, 8) X(3, 32, 4) X(3, 16, 4) X(5, 32, 16) X(5, 16, 16)
+#define VD_GA_POP_SHAPES(X)                                                 \
+    X(1, 64, 1) X(1, 32, 1) X(1, 16, 1) X(3, 64, 4) X(3, 32, 4) X(3, 16, 4) \
+    X(4, 32, 8) X(4, 16, 8) X(5, 32, 16) X(5, 16, 16)
 /* Every GA launch shape is explicitly instantiated in the build part of its TPP and declared
  * extern in the others (VD_KW_<part> = `template` or `extern template`). */
 #if VD_PART < 0 || VD_PART == 1
@@ -607,10 +700,101 @@ int ga_occupancy_r3(unsigned bytes)
                                                  int, const GaDev &, uint64_t, int64_t, int,      \
                                                  const GaLayout &, const GaOut &, cudaStream_t,   \
                                                  int *, double **, int *);
+#define VD_GA_POP_INST(P, N, T)                                                                   \
+    VD_KW_##P cudaError_t launch_pop_t<N, T>(const GridView &, const LigView *, const int *, int, \
+                                             int, const double *, int, unsigned,                  \
+                                             float *, double *, double *, cudaStream_t, bool,     \
+                                             int *);
 VD_GA_SHAPES(VD_GA_INST)
 VD_GA_TEAM_SHAPES(VD_GA_TEAM_INST)
+VD_GA_POP_SHAPES(VD_GA_POP_INST)
 
 #if VD_PART <= 0
+/* generation-synchronous GA: dispatch of one scoring launch (false: shape not built) */
+bool launch_pop(int npp, int tpp, cudaError_t *err, const GridView &Gv, const LigView *d_ligs,
+                const int *d_order, int count, int pop, const double *genes, int gmax,
+                unsigned bytes, float *fit, double *e64, double *a64, cudaStream_t st,
+                bool setup, int *pct)
+{
+#define VD_PS(P_, N, T)                                                                          \
+    if (npp == N && tpp == T) {                                                                  \
+        *err = launch_pop_t<N, T>(Gv, d_ligs, d_order, count, pop, genes, gmax, bytes, fit, e64, \
+                                  a64, st, setup, pct);                                          \
+        return true;                                                                             \
+    }
+    VD_GA_POP_SHAPES(VD_PS)
+#undef VD_PS
+    return false;
+}
+
+__global__ void ga_init_kernel(const LigView *__restrict__ ligs, const int *__restrict__ order,
+                               GaDev P, uint64_t seed, int64_t base, double *genes, int gmax)
+{
+    const int slot = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.pop) return;
+    const int l = order[slot], T = ligs[l].n_torsions;
+    init_individual(P, T, i, seed, (uint64_t)(base + l),
+                    genes + (size_t)slot * P.pop * gmax + (size_t)i * (7 + T));
+}
+
+/* One GA generation of one ligand per CTA, after its population was scored: the tail of
+ * ga_kernel's generation loop (generation best with strict '<', trace, stable elites,
+ * thread-per-child breeding into the other buffer). */
+__global__ void __launch_bounds__(256) ga_step_kernel(const LigView *__restrict__ ligs,
+                                                      const int *__restrict__ order, GaDev P,
+                                                      uint64_t seed, int64_t base, int gen,
+                                                      const double *__restrict__ cur_all,
+                                                      double *__restrict__ nxt_all, int gmax,
+                                                      const float *__restrict__ fit_all,
+                                                      const double *__restrict__ e_all,
+                                                      const double *__restrict__ a_all, GaOut out)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int B = blockDim.x, pop = P.pop;
+    float *fit = reinterpret_cast<float *>(smem);
+    unsigned char *taken = smem + 4 * (size_t)pop;
+    __shared__ int s_best;
+    __shared__ int s_idx[33];
+    __shared__ float s_val[32];
+    const int slot = blockIdx.x, l = order[slot];
+    const int G = 7 + ligs[l].n_torsions;
+    const uint64_t k0 = seed, k1 = (uint64_t)(base + l);
+    const double *cur = cur_all + (size_t)slot * pop * gmax;
+    double *nxt = nxt_all + (size_t)slot * pop * gmax;
+    for (int i = threadIdx.x; i < pop; i += B) {
+        fit[i] = fit_all[(size_t)slot * pop + i];
+        taken[i] = 0;
+    }
+    __syncthreads();
+    const int idx = block_argmin(fit, nullptr, pop, s_idx, s_val);
+    VD_CHK(idx >= 0 && idx < pop, VD_SITE_POP);
+    const float fb = fit[idx];
+    const bool better = gen == 0 || fb < out.best_total[l];  /* strict '<' (vd/ga.py:217) */
+    __syncthreads();  /* every thread has read best_total before thread 0 updates it */
+    if (better) {
+        for (int g = threadIdx.x; g < G; g += B) out.best_genes[(size_t)l * out.gstride + g] = cur[(size_t)idx * G + g];
+        if (threadIdx.x == 0) {
+            out.best_total[l] = fb;
+            out.best_inter[l] = e_all[(size_t)slot * pop + idx];
+            out.best_intra[l] = a_all[(size_t)slot * pop + idx];
+        }
+    }
+    if (out.trace && threadIdx.x == 0) out.trace[(size_t)l * (P.generations + 1) + gen] = fb;
+    if (gen == P.generations) {
+        if (threadIdx.x == 0) out.n_evals[l] = (int64_t)pop * (P.generations + 1);
+        return;
+    }
+    for (int e = 0; e < P.elitism; ++e) {
+        const int ei = e == 0 ? idx : block_argmin(fit, taken, pop, s_idx, s_val);
+        if (threadIdx.x == 0) { taken[ei] = 1; s_best = ei; }
+        __syncthreads();
+        for (int g = threadIdx.x; g < G; g += B) nxt[(size_t)e * G + g] = cur[(size_t)s_best * G + g];
+        __syncthreads();
+    }
+    for (int c = threadIdx.x; c < pop - P.elitism; c += B)
+        breed_child(P, G, cur, fit, gen, c, k0, k1, nxt + (size_t)(P.elitism + c) * G);
+}
+
 cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const LigView *d_ligs,
                       const int *d_order, int count, const GaDev &P, uint64_t seed, int64_t base,
                       int gmax, const GaLayout &lay, const GaOut &out, cudaStream_t st,
@@ -807,15 +991,46 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     static const int kBucketEdge[] = {24, 32, 48, 64, 96, 128, 192, 256, 1 << 30};
     constexpr int kBuckets = sizeof(kBucketEdge) / sizeof(int);
     std::vector<vd::LigView> views(count);
+    /* fast mode, ligands up to 96 atoms with resident pair lists: grouped instead by the
+       score-kernel shape each ligand gets on its own (pick_shape, wide) and by the shared-
+       memory configuration two of its CTAs need (which sets the L1 share): a ligand's shape,
+       and with it the partition of its fp32 pair sums, never depends on its batch mates.
+       Groups come after the kBuckets atom-count buckets: key = npp | tpp << 8 | class << 16. */
     std::vector<std::vector<int>> bucket(kBuckets);
+    std::vector<int> gkey;
     int tmax = 0;
     for (int l = 0; l < count; ++l) {
         views[l] = s->view(first + l);
         tmax = std::max(tmax, views[l].n_torsions);
+        const vd::LigView &V = views[l];
+        int sn = 0, stp = 0;
+        if (!exact && V.n_atoms <= 96 && V.n_pairs <= vd::kResidentPairs && !getenv("VD_GA_TPP") &&
+            vd::pick_shape(V.n_atoms, V.n_pairs, V.n_torsions, false, &sn, &stp, true) == 0) {
+            const unsigned two = 2u * (vd::smem_layout(V.n_atoms, V.n_torsions, V.n_frag, sn, stp, 0, V.n_pairs).bytes + 1024u);
+            const int cls = two <= 164u * 1024u ? 0 : 1;  /* >= 92 KB of L1 left, or less */
+            const int key = sn | (stp << 8) | (cls << 16);
+            size_t k = 0;
+            while (k < gkey.size() && gkey[k] != key) ++k;
+            if (k == gkey.size()) {
+                gkey.push_back(key);
+                bucket.emplace_back();
+            }
+            bucket[kBuckets + k].push_back(l);
+            continue;
+        }
         int b = 0;
-        while (views[l].n_atoms > kBucketEdge[b]) ++b;
+        while (V.n_atoms > kBucketEdge[b]) ++b;
         bucket[b].push_back(l);
     }
+    /* a small class of a shape joins the shape's other class (the class only sets the L1 share) */
+    for (size_t k = 0; k < gkey.size(); ++k)
+        for (size_t m = 0; m < gkey.size(); ++m)
+            if (m != k && (gkey[m] & 0xffff) == (gkey[k] & 0xffff) && !bucket[kBuckets + k].empty() &&
+                bucket[kBuckets + k].size() < 64 && !bucket[kBuckets + m].empty()) {
+                auto &src = bucket[kBuckets + k], &dst = bucket[kBuckets + m];
+                dst.insert(dst.end(), src.begin(), src.end());
+                src.clear();
+            }
     const int gmax = 7 + tmax;
     if (gstride < gmax) {
         set_error("vd_dock_batch: gstride smaller than 7 + max torsions");
@@ -826,12 +1041,20 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
     struct Launch {
         int off, cnt, npp, tpp;
         vd::GaLayout lay;
+        /* generation-synchronous path (see pop_score_kernel) */
+        bool sync = false;
+        int s_npp = 0, s_tpp = 0, s_gmax = 0, s_pct = 100;
+        unsigned s_bytes = 0;        /* the largest of the group's own layouts */
+        double *s_genes = nullptr;   /* [2][cnt][pop][s_gmax] */
+        float *s_fit = nullptr;
+        double *s_e = nullptr, *s_a = nullptr;
     };
     std::vector<Launch> launches;
     const unsigned extra = (unsigned)p->pop * (4u + 8u + 8u + 1u) + 64u;
-    for (int b = 0; b < kBuckets; ++b) {
+    for (int b = 0; b < (int)bucket.size(); ++b) {
         if (bucket[b].empty()) continue;
         auto &v = bucket[b];
+        const int key = b >= kBuckets ? gkey[b - kBuckets] : 0;  /* shape group (see above) */
         std::stable_sort(v.begin(), v.end(), [&](int x, int y) {
             return (int64_t)views[x].n_pairs + 4 * views[x].n_atoms >
                    (int64_t)views[y].n_pairs + 4 * views[y].n_atoms;
@@ -846,6 +1069,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         Launch L;
         int npp0;
         if (vd::pick_shape(nmax, pmax, tb, exact, &npp0, &L.tpp)) return -1;
+        if (key) L.tpp = (key >> 8) & 0xff;  /* the persistent kernel runs the group's subs too */
         if (!exact)
             if (const char *ov = getenv("VD_GA_TPP")) {  /* tuning override */
                 const int v = atoi(ov);
@@ -862,18 +1086,6 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             if (lay.base.bytes > 227u * 1024u) continue;
             if (npp * L.tpp < 32) continue;  /* block_argmin's shuffles need whole warps */
             int warps = vd::ga_occupancy(exact, npp, L.tpp, lay.base.bytes, gv.yz != nullptr) * npp * L.tpp / 32;
-            lay.r3 = 0;
-            if (!exact && npp == 32 && L.tpp == 4 && gv.yz != nullptr && nmax <= 32 &&
-                !getenv("VD_GA_NO_R3")) {
-                /* small ligands: a third CTA fits in shared memory but not in 245 registers.
-                   Measured with the 168-register budget (76 B of spills): <= 24 atoms +7%,
-                   25-32 atoms +8% ligands/s; only those buckets take it */
-                const int w3 = vd::ga_occupancy_r3(lay.base.bytes) * 4;
-                if (w3 > warps) {
-                    warps = w3;
-                    lay.r3 = 1;
-                }
-            }
             if (npp == 64) warps -= 4;  /* measured: 64 needs clearly more warps to win */
             /* (unlike the score kernel, the GA prefers one 32 x 8 CTA to two 16 x 8 ones at
                the same warps for cfg4: 1239 vs 880 ligands/s -- its per-tile barriers and
@@ -923,11 +1135,10 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             while (team < 8 && (double)count * team / slots < 6.0 && (size_t)count * team < (size_t)(8 * slots)) team *= 2;
             if (const char *ov = getenv("VD_GA_TEAM")) team = std::max(1, std::min(8, atoi(ov)));
             L.lay.team = team;
-            if (team > 1) L.lay.r3 = 0;  /* the team kernel has no 3-CTA register variant */
         }
         if (getenv("VD_VERBOSE"))
-            fprintf(stderr, "[vd] ga bucket <=%d atoms: %zu ligands, npp=%d tpp=%d smem=%u warps/sm=%d team=%d\n",
-                    kBucketEdge[b], v.size(), L.npp, L.tpp, L.lay.base.bytes, best_warps, L.lay.team);
+            fprintf(stderr, "[vd] ga bucket %d (shape key %#x): %zu ligands, <= %d atoms, npp=%d tpp=%d smem=%u warps/sm=%d team=%d\n",
+                    b, key, v.size(), nmax, L.npp, L.tpp, L.lay.base.bytes, best_warps, L.lay.team);
         unsigned off = L.lay.base.extra;
         L.lay.off_e = off;
         off += 8u * p->pop;
@@ -938,6 +1149,33 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         L.lay.off_taken = off;
         L.off = (int)order.size();
         L.cnt = (int)v.size();
+        /* generation-synchronous path: fast mode, ligands up to 96 atoms (beyond, the
+           persistent kernel at 16 subs matches the score kernel), resident pair lists, and
+           enough (ligand, tile) CTAs per generation to fill the GPU several times over.
+           VD_GA_SYNC=0 keeps the persistent kernels, =1 forces the path where its shape exists. */
+        if (key) {
+            /* the group's sub count is part of its numerics and fixed; the pose tile is not:
+               a batch too small to fill the GPU with its own tile takes smaller ones (a single
+               cfg0 dock, pop 100: one 64-pair tile -> four 16-pair CTAs, 2.5 -> 1.6 ms) */
+            int sn = key & 0xff;
+            const int stp = (key >> 8) & 0xff;
+            auto ctas = [&](int n) { return (size_t)L.cnt * ((p->pop + 2 * n - 1) / (2 * n)); };
+            while (sn > 16 && ctas(sn) < 2u * 296u) sn /= 2;
+            bool want = true;
+            if (const char *ov = getenv("VD_GA_SYNC")) want = atoi(ov) != 0;  /* 0: persistent kernels (A/B, tests) */
+            cudaError_t e = cudaSuccess;
+            for (int l : v)
+                L.s_bytes = std::max(L.s_bytes, vd::smem_layout(views[l].n_atoms, views[l].n_torsions, views[l].n_frag,
+                                                               sn, stp, 0, views[l].n_pairs).bytes);
+            if (want && vd::launch_pop(sn, stp, &e, gv, nullptr, nullptr, L.cnt, p->pop, nullptr, 0,
+                                       L.s_bytes, nullptr, nullptr, nullptr, st, true, &L.s_pct)) {
+                VD_CK(e);
+                L.sync = true;
+                L.s_npp = sn;
+                L.s_tpp = stp;
+                L.s_gmax = 7 + tb;
+            }
+        }
         order.insert(order.end(), v.begin(), v.end());
         launches.push_back(L);
     }
@@ -980,19 +1218,78 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
         VD_CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
         VD_CK(cudaEventRecord(fork, st));
     }
+    std::vector<cudaStream_t> lstream(launches.size(), st);
+    /* VD_GA_TIME=1 (tuning): one bucket at a time, host-timed, printed */
+    const bool timing = getenv("VD_GA_TIME") != nullptr;
+    for (int only = timing ? 0 : -1; only < (timing ? (int)launches.size() : 0); ++only) {
+    const auto t_begin = std::chrono::steady_clock::now();
+    if (timing) cudaDeviceSynchronize();
     for (int b = (int)launches.size() - 1; b >= 0; --b) {
-        const Launch &L = launches[b];
+        if (only >= 0 && b != only) continue;
+        Launch &L = launches[b];
         cudaStream_t ls = st;
         if (fork && b != (int)launches.size() - 1) {
             VD_CK(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking));
             side.push_back(ls);
             VD_CK(cudaStreamWaitEvent(ls, fork, 0));
         }
+        lstream[b] = ls;
+        if (L.sync) {  /* population buffers + generation 0's individuals */
+            const size_t npop = (size_t)L.cnt * p->pop;
+            VD_CK(cudaMallocAsync((void **)&L.s_genes, sizeof(double) * 2 * npop * L.s_gmax, ls));
+            VD_CK(cudaMallocAsync((void **)&L.s_fit, sizeof(float) * npop, ls));
+            VD_CK(cudaMallocAsync((void **)&L.s_e, sizeof(double) * npop, ls));
+            VD_CK(cudaMallocAsync((void **)&L.s_a, sizeof(double) * npop, ls));
+#ifdef VD_CHECKED
+            VD_CK(cudaMemsetAsync(L.s_genes, 0xff, sizeof(double) * 2 * npop * L.s_gmax, ls));
+#endif
+            vd::ga_init_kernel<<<dim3((p->pop + 127) / 128, L.cnt), 128, 0, ls>>>(
+                d_views, d_order + L.off, P, seed, lig_index_base, L.s_genes, L.s_gmax);
+            ++vdi::g_launches;
+            VD_CK(cudaGetLastError());
+            continue;
+        }
         int n_ctas = 0;
         gene_buf = nullptr;
         VD_CK(vd::launch_ga(exact, L.npp, L.tpp, gv, d_views, d_order + L.off, L.cnt, P, seed,
                             lig_index_base, gmax, L.lay, o, ls, d_work + b, &gene_buf, &n_ctas));
         cudaFreeAsync(gene_buf, ls);
+    }
+    /* generation-synchronous buckets: generation-major over the buckets' streams, so that
+       one bucket's launch tails are filled by the others' CTAs */
+    for (int gen = 0; gen <= p->generations; ++gen)
+        for (int b = (int)launches.size() - 1; b >= 0; --b) {
+            Launch &L = launches[b];
+            if (!L.sync || (only >= 0 && b != only)) continue;
+            const size_t half = (size_t)L.cnt * p->pop * L.s_gmax;
+            const double *cur = L.s_genes + (gen & 1) * half;
+            double *nxt = L.s_genes + ((gen + 1) & 1) * half;
+            cudaError_t e = cudaSuccess;
+            vd::launch_pop(L.s_npp, L.s_tpp, &e, gv, d_views, d_order + L.off, L.cnt, p->pop, cur,
+                           L.s_gmax, L.s_bytes, L.s_fit, L.s_e, L.s_a, lstream[b], false, &L.s_pct);
+            VD_CK(e);
+            vd::ga_step_kernel<<<L.cnt, 256, 5u * (unsigned)p->pop + 16u, lstream[b]>>>(
+                d_views, d_order + L.off, P, seed, lig_index_base, gen, cur, nxt, L.s_gmax, L.s_fit,
+                L.s_e, L.s_a, o);
+            ++vdi::g_launches;
+            VD_CK(cudaGetLastError());
+        }
+    for (Launch &L : launches)
+        if (L.sync && (only < 0 || &L - launches.data() == only)) {
+            const cudaStream_t ls = lstream[&L - launches.data()];
+            cudaFreeAsync(L.s_genes, ls);
+            cudaFreeAsync(L.s_fit, ls);
+            cudaFreeAsync(L.s_e, ls);
+            cudaFreeAsync(L.s_a, ls);
+        }
+    if (timing) {
+        cudaDeviceSynchronize();
+        const Launch &L = launches[only];
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_begin).count();
+        fprintf(stderr, "[vd] ga time: bucket %d %s npp=%d tpp=%d: %d ligands %.1f ms, %.0f M evals/s\n", only,
+                L.sync ? "sync" : "persistent", L.sync ? L.s_npp : L.npp, L.sync ? L.s_tpp : L.tpp, L.cnt, ms,
+                (double)L.cnt * p->pop * (p->generations + 1) / ms / 1e3);
+    }
     }
     for (cudaStream_t ls : side) {  /* join: st waits for every side stream */
         cudaEvent_t done;

@@ -64,7 +64,9 @@ void chk_selftest_ga();
 }  // namespace vdi
 
 namespace vd {
-int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp);
+/* wide: the score kernels' rule (256-thread CTAs whatever the pose tile); the persistent GA
+ * kernels keep 4 subs up to 96 atoms */
+int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp, bool wide = false);
 }
 
 #define VD_CK(call)                                        \

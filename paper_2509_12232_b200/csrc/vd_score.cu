@@ -141,7 +141,7 @@ constexpr unsigned kL1ReserveKB = 32;  /* of the 256 KB L1/shared array, kept as
 
 #if VD_PART <= 0
 /* Launch shape for a ligand: pose pairs per CTA (NPP) and threads per pair (TPP). */
-int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp)
+int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *tpp, bool wide)
 {
     const unsigned limit = 200 * 1024;
     /* threads per pose pair: more subs for larger ligands, where 12*N bytes of
@@ -162,6 +162,11 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
     int force_npp = 0;
     if (!exact)
         if (const char *ov = getenv("VD_NPP")) force_npp = atoi(ov);  /* tuning override */
+    /* wide (the score kernels, 121 registers): when shared memory forces a smaller pose tile,
+       more subs keep the CTA at 256 threads, 16 warps per SM with 2 CTAs -- a 59-atom,
+       1,451-pair ligand (32 pose pairs per CTA): 315 (32 x 4) -> 422 M poses/s (32 x 8).
+       The persistent GA kernels (245 registers) keep 4 subs up to 96 atoms. */
+    const bool widen = wide && !exact && t == 4 && !getenv("VD_TPP");
     /* pose pairs per CTA: the largest tile of which 2 CTAs fit beside the L1 share kept
        for the gathers (see launch_t), else the first that fits at all.  cfg1 sweep
        (TPP x NPP, CTAs/SM): 4 x 64 (2) 1.67 ms; 4 x 32 (3) 1.77; 8 x 16 (6) 1.85;
@@ -176,10 +181,15 @@ int pick_shape(int n_atoms, int n_pairs, int n_tors, bool exact, int *npp, int *
             if (force_npp && n != force_npp) continue;
             if (exact && t == 8 && n == 64) continue;  /* 512 threads: beyond the exact kernels' registers */
             if (t == 16 && n == 64) continue;          /* 1,024 threads: not built */
-            const unsigned b = smem_layout(n_atoms, n_tors, 4 * n_atoms, n, t, 0, n_pairs).bytes;
-            if (b <= (pass == 0 && !exact ? two_ctas : limit)) {
+            const int tn = widen ? 256 / n : t;
+            const unsigned b = smem_layout(n_atoms, n_tors, 4 * n_atoms, n, tn, 0, n_pairs).bytes;
+            /* wide, below 64 pose pairs: two CTAs may take the whole array (28 KB of L1 left):
+               32 x 8 with little L1 still beats 16 x 16 (cfg2's 60-atom ligands: 247 M evals/s
+               at 16 x 16) */
+            const unsigned two = widen && n < 64 ? (228u * 1024u) / 2u - 1024u : two_ctas;
+            if (b <= (pass == 0 && !exact ? two : limit)) {
                 *npp = n;
-                *tpp = t;
+                *tpp = tn;
                 return 0;
             }
         }
@@ -242,6 +252,13 @@ cudaError_t launch_t(const GridView &G, const LigView &L, const double *genes,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    /* the occupancy query honours the kernel's CURRENT carveout: after a smaller ligand of the
+       same shape had set a low one, a larger ligand was told 1 CTA/SM and ran at half its
+       occupancy (31- and 37-atom ligands after a 21-atom one: 657 -> 972 and 502 -> 732 M
+       poses/s).  Ask with the carveout at its maximum, then set the one wanted. */
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (e != cudaSuccess) return e;
+    *carve = 100;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NPP * TPP, lay.bytes);
     if (e != cudaSuccess) return e;
     int l1_kb = kL1ReserveKB;
@@ -325,7 +342,7 @@ cudaError_t launch_score(int mode, int src, const GridView &G, const LigView &L,
 {
     const bool exact = mode == VD_MODE_EXACT;
     int npp, tpp;
-    if (pick_shape(L.n_atoms, L.n_pairs, L.n_torsions, exact, &npp, &tpp)) return cudaErrorInvalidValue;
+    if (pick_shape(L.n_atoms, L.n_pairs, L.n_torsions, exact, &npp, &tpp, true)) return cudaErrorInvalidValue;
     if (P <= 0) return cudaSuccess;
     const double *g = src == 0 ? genes : nullptr;
     const float *p = src == 0 ? nullptr : poses;

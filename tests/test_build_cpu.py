@@ -38,17 +38,18 @@ def test_score_kernel_fits_two_ctas_without_spills(kernel):
 
 
 @pytest.mark.parametrize("kernel", [
-    "_ZN2vd9ga_kernelILb0ELi32ELi4ELi1E",   # cfg2 buckets, packed grid
-    "_ZN2vd9ga_kernelILb0ELi32ELi8ELi2E",   # cfg4, plain grid
+    "_ZN2vd16pop_score_kernelILi64ELi4ELi1E",   # generation-synchronous GA, cfg2 shapes
+    "_ZN2vd16pop_score_kernelILi32ELi8ELi1E",
 ])
-def test_ga_kernel_has_no_spills(kernel):
+def test_pop_score_kernel_fits_two_ctas_without_spills(kernel):
     regs, spill = _resources(kernel)
-    assert spill == 0, f"{kernel}: {spill} bytes of spills at {regs} registers"
+    assert regs <= 128, f"{kernel}: {regs} registers (2 CTAs x 256 threads need <= 128)"
+    assert spill == 0, f"{kernel}: {spill} bytes of spills"
 
 
-def test_ga_r3_variant_spills_stay_bounded():
-    """The 3-CTA register-budget GA variant (LAY 3, 168 registers; chosen only for packed
-    buckets of <= 32 atoms, where it measured +7-8%) spills a little by design: bound it."""
-    regs, spill = _resources("_ZN2vd9ga_kernelILb0ELi32ELi4ELi3E")
-    assert regs <= 168, regs
-    assert spill <= 128, f"{spill} bytes of spill stores at {regs} registers"
+def test_cfg4_ga_kernel_spills_stay_bounded():
+    """The cfg4 persistent GA kernel (32 x 16 subs, 512 threads) is compiled to 128 registers;
+    a few bytes of spills are the price, more would show in the stress leg."""
+    regs, spill = _resources("_ZN2vd9ga_kernelILb0ELi32ELi16ELi2E")
+    assert regs <= 128, regs
+    assert spill <= 64, f"{spill} bytes of spill stores at {regs} registers"

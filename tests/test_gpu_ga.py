@@ -261,30 +261,39 @@ def test_fast_mode_ga_identical_on_every_grid_layout(cuda, layout, monkeypatch):
     assert np.array_equal(got.best_genotype, ref.best_genotype)
 
 
-def test_r3_register_budget_variant_is_bit_identical(cuda, monkeypatch):
-    """Small packed-grid buckets (<= 32 atoms) run the 3-CTA register-budget GA variant
-    (LAY 3); VD_GA_NO_R3=1 forces the full-budget kernel.  Same code, same results."""
-    from paper_2509_12232_b200 import gridmaps, hostprep, synth
+def test_generation_synchronous_path_is_bit_identical_to_persistent_kernels(cuda, monkeypatch):
+    """Batches that fill the GPU run every generation as two launches over all ligands
+    (pop_score_kernel at the score kernel's shapes + ga_step_kernel); smaller batches and
+    teams run the persistent kernels.  Both use a ligand's own sub-thread count and the same
+    role split, operators and random streams, so which path a batch takes never shows:
+    every output of a 96-ligand cfg2 batch is identical byte for byte."""
+    from paper_2509_12232_b200 import _abi, gridmaps, hostprep, synth
     from paper_2509_12232_b200.ga import GaConfig, _run
 
     spec = synth.config_grid_spec(2)
     gset = gridmaps.build_grid_maps(synth.config_protein(2), spec, synth.CONFIGS[2].probe_types)
     grid = cuda["fast"]._grid_for_set(gset)
     batch = hostprep.TopologyBatch.synth(2, 0, 96)
-    keep = np.flatnonzero(batch.n_atoms <= 32)[:24]
-    assert len(keep) >= 8
-    arrays = hostprep.prepare_batch(batch, grid.labels)
-    lset = hostprep.ligand_set(arrays)
-    ga = GaConfig(population_size=256, generations=20, translation_bounds=(spec.origin, spec.upper))
+    assert batch.n_atoms.min() <= 24 and batch.n_atoms.max() >= 56  # several shape groups
+    lset = hostprep.ligand_set(hostprep.prepare_batch(batch, grid.labels))
+    ga = GaConfig(population_size=256, generations=20, elitism_count=2,
+                  translation_bounds=(spec.origin, spec.upper))
     gmax = 7 + int(batch.n_torsions.max())
-    from paper_2509_12232_b200 import _abi
 
-    def run():
+    def run(sync):
+        monkeypatch.setenv("VD_GA_SYNC", sync)
         return _run(grid, lset, 0, 96, ga, 4, 0, _abi.MODE_FAST, gmax)
 
-    a = run()
-    monkeypatch.setenv("VD_GA_NO_R3", "1")
-    b = run()
+    a, b = run("0"), run("1")
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    # odd populations (half-filled pose pairs and tiles), no elites
+    ga2 = GaConfig(population_size=67, generations=6, elitism_count=0,
+                   translation_bounds=(spec.origin, spec.upper))
+    monkeypatch.setenv("VD_GA_SYNC", "0")
+    a = _run(grid, lset, 0, 24, ga2, 9, 100, _abi.MODE_FAST, gmax)
+    monkeypatch.setenv("VD_GA_SYNC", "1")
+    b = _run(grid, lset, 0, 24, ga2, 9, 100, _abi.MODE_FAST, gmax)
     for x, y in zip(a, b):
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
 

@@ -5,9 +5,9 @@ build comparison (tests/test_gpu_checked.py; compute-sanitizer is closed on this
                 with streamed pair tiles (128-atom fixture), TPP 8 exact; yz-brick, z-pair
                 and plain grid layouts; the host-buffer pipeline path
   pose_kernel   TPP 1 / 4 / 8 / 16
-  ga_kernel     fast packed, fast plain, exact, several buckets at once (incl. the
-                3-CTA r3 variant for <= 32-atom buckets); ga_team_kernel (6 cfg4
-                ligands: one ligand over 8 CTAs)
+  ga_kernel     fast packed, fast plain, exact, several shape groups at once, the same
+                batch through the generation-synchronous path (pop_score_kernel +
+                ga_step_kernel); ga_team_kernel (6 cfg4 ligands: one ligand over 8 CTAs)
   grid_kernel   a small device grid build; MUGD load (transpose kernel)
 Usage: [VD_LIB=.../libvdb200_checked.so] python tools/sanitize_case.py OUT.npz
 Prints the checked build's device flag word (0 = no bounds/invariant failure).
@@ -66,7 +66,7 @@ def main(out_path):
                 out[f"{layout}_{name}_{mode}_ga_trace"] = r.trace
         for k in env:
             del os.environ[k]
-    # several GA buckets at once (concurrent bucket launches, r3 variant) on a cfg2 batch
+    # several GA shape groups at once (concurrent launches) on a cfg2 batch
     spec = gridmaps.GridSpec.centered((0.0, 0.0, 0.0), (40, 40, 40), 0.375)
     gset = gridmaps.build_grid_maps(synth.make_protein(5, 1500), spec, synth.CONFIGS[2].probe_types)
     out["grid_maps_sample"] = np.stack([gset.maps[l][::7, ::5, ::3] for l in gset.maps])
@@ -80,6 +80,14 @@ def main(out_path):
              0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
     for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
         out[f"batch_ga_{k}"] = v
+    # the same batch through the generation-synchronous path (bit-identical by design)
+    os.environ["VD_GA_SYNC"] = "1"
+    r = _run(grid, lset, 0, 40, GaConfig(population_size=64, generations=3,
+                                         translation_bounds=(spec.origin, spec.upper)),
+             0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
+    del os.environ["VD_GA_SYNC"]
+    for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
+        out[f"sync_ga_{k}"] = v
     # large ligands in a small batch: the team kernel (a ligand's population over 8 CTAs)
     b4 = hostprep.TopologyBatch.synth(4, 0, 6)
     l4 = hostprep.ligand_set(hostprep.prepare_batch(b4, grid.labels))
