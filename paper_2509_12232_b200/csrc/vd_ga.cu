@@ -740,7 +740,7 @@ __global__ void ga_init_kernel(const LigView *__restrict__ ligs, const int *__re
 /* One GA generation of one ligand per CTA, after its population was scored: the tail of
  * ga_kernel's generation loop (generation best with strict '<', trace, stable elites,
  * thread-per-child breeding into the other buffer). */
-__global__ void __launch_bounds__(256) ga_step_kernel(const LigView *__restrict__ ligs,
+__global__ void __launch_bounds__(256, 4) ga_step_kernel(const LigView *__restrict__ ligs,
                                                       const int *__restrict__ order, GaDev P,
                                                       uint64_t seed, int64_t base, int gen,
                                                       const double *__restrict__ cur_all,

@@ -263,7 +263,8 @@ cudaError_t launch_t(const GridView &G, const LigView &L, const double *genes,
     if (e != cudaSuccess) return e;
     int l1_kb = kL1ReserveKB;
     if (const char *w = getenv("VD_L1_KB")) l1_kb = atoi(w);  /* tuning override */
-    const int fit = (smem_sm - l1_kb * 1024) / (int)(lay.bytes + resv);
+    int fit = (smem_sm - l1_kb * 1024) / (int)(lay.bytes + resv);
+    if (fit < 2) fit = std::min(2, smem_sm / (int)(lay.bytes + resv));  /* two CTAs beat the L1 share */
     const int want = std::max(1, std::min(occ, fit));
     int pct = (int)((100LL * want * (lay.bytes + resv) + smem_sm - 1) / smem_sm);
     if (const char *cv = getenv("VD_CARVEOUT")) pct = atoi(cv);  /* tuning override */
