@@ -1171,7 +1171,8 @@ template <bool EXACT, int NPP, int TPP, bool PIPE, bool SPLIT, int LAY = 0, bool
           bool ASYNC = false>
 __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, const float2 *S,
                                         const PairTile &T, int sub, double &e0, double &e1,
-                                        double &a0, double &a1, double *red = nullptr, int pp = 0)
+                                        double &a0, double &a1, double *red = nullptr, int pp = 0,
+                                        float split_r = kSplitR)
 {
     if constexpr (EXACT && TPP > 1) {
         /* inter: sub 0 alone, atoms in order (a sequential fp64 sum); intra: the 8 reference
@@ -1197,9 +1198,9 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
            after them, R = 14/16/18.5/21.7/26/30/36/45 gave 1.553/1.501/1.458/1.435/1.419/
            1.442/1.462/1.484 ms, so R = 26 (xa = 8). */
         const int n = L.n_atoms, np = L.n_pairs;
-        const float ex = (float)n - (float)np * (1.0f / kSplitR);
+        const float ex = (float)n - (float)np * (1.0f / split_r);
         const int xa = ex > 0.f ? min(n, (int)(0.5f * ex + 0.5f)) : 0;
-        const unsigned px = ex < 0.f ? (unsigned)(-ex * kSplitR / (2.0f * (float)np) * 65536.0f) : 0u;
+        const unsigned px = ex < 0.f ? (unsigned)(-ex * split_r / (2.0f * (float)np) * 65536.0f) : 0u;
         const int acut = n - xa;
         if (sub < NI) {
             inter2<EXACT, NPP, NI, PIPE, LAY, FLAT>(L, G, S, sub, 0, acut, e0, e1);

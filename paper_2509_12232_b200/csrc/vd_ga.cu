@@ -200,6 +200,12 @@ struct GaTeam {
    atoms); the 16-sub kernels (cfg4: streamed pair lists, which never split) stay without
    the split code, which cost them 780 B of spills */
 __host__ __device__ constexpr bool ga_split(int tpp) { return VD_GA_SPLIT != 0 && tpp <= 8; }
+/* role-split balance of the GA paths: a GA population sits in the box (every atom gathers),
+   so one atom's gathers weigh more pair terms than under cfg1's random poses (kSplitR) */
+#ifndef VD_GA_SPLIT_R
+#define VD_GA_SPLIT_R 26.0f
+#endif
+constexpr float kGaSplitR = VD_GA_SPLIT_R;
 constexpr int ga_minb(int threads)
 {
     return VD_GA_REGS > 0 ? (65536 / (threads * VD_GA_REGS) > 0 ? 65536 / (threads * VD_GA_REGS) : 1)
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(NPP *TPP, EXACT ? VD_GA_EXACT_MINB : ga_minb(N
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, ga_split(TPP), LAY, false, true>(
-                    L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
+                    L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp, kGaSplitR);
                 reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < pop) { e64[i0] = e0; a64[i0] = a0; fit[i0] = total32(e0, a0, L.tors32); }
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
                 if (TPP > 1) __syncthreads();
                 double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
                 energy2<EXACT, NPP, TPP, VD_GA_PIPE != 0, ga_split(TPP), LAY, false, true>(
-                    L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp);
+                    L, Gv, S, Tl, sub, e0, e1, a0, a1, red, pp, kGaSplitR);
                 reduce_subs<NPP, TPP, EXACT>(red, pp, sub, e0, e1, a0, a1);
                 if (sub == 0) {
                     if (i0 < i_hi) { ge[i0] = e0; ga[i0] = a0; gfit[i0] = total32(e0, a0, L.tors32); }
@@ -488,7 +494,7 @@ __global__ void __launch_bounds__(NPP *TPP) pop_score_kernel(GridView G, const L
     if (TPP > 1) __syncthreads();
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
     energy2<false, NPP, TPP, false, ga_split(TPP), LAY>(L, G, S, T, sub, e0, e1, a0, a1,
-                                               reinterpret_cast<double *>(smem + lay.red), pp);
+                                               reinterpret_cast<double *>(smem + lay.red), pp, kGaSplitR);
     reduce_subs<NPP, TPP, false>(reinterpret_cast<double *>(smem + lay.red), pp, sub, e0, e1, a0, a1);
     if (sub == 0) {
         const size_t o = (size_t)slot * pop;
