@@ -42,8 +42,8 @@ WORKLOAD = "cfg1-score-1M"
 FP32_SPEC_TFLOPS = 2 * 128 * 148 * 1.965e9 / 1e12  # 74.4, spec-derived (no measured FP32 peak)
 # dram__bytes_read.sum + dram__bytes_write.sum of one score_kernel launch (1M poses) from the
 # committed ncu --set full capture; algorithmic HBM bytes = 120 MB genes + 20 MB results
-TRAFFIC_BYTES = 166.15e6 + 21.19e6
-TRAFFIC_SRC = "profiles/r2_score.md (ncu --set full, one launch of score_kernel<0,64,4,1>)"
+TRAFFIC_BYTES = 166.14e6 + 20.66e6
+TRAFFIC_SRC = "profiles/r2c_score.md (ncu --set full, one launch of score_kernel<0,64,4,1>)"
 
 
 def env_int(k, d):

@@ -736,7 +736,7 @@ bool launch_pop(int npp, int tpp, cudaError_t *err, const GridView &Gv, const Li
 __global__ void ga_init_kernel(const LigView *__restrict__ ligs, const int *__restrict__ order,
                                GaDev P, uint64_t seed, int64_t base, double *genes, int gmax)
 {
-    const int slot = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int slot = blockIdx.x, i = blockIdx.y * blockDim.x + threadIdx.x;  /* x: up to 2^31 - 1 ligands */
     if (i >= P.pop) return;
     const int l = order[slot], T = ligs[l].n_torsions;
     init_individual(P, T, i, seed, (uint64_t)(base + l),
@@ -1167,8 +1167,14 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
             const int stp = (key >> 8) & 0xff;
             auto ctas = [&](int n) { return (size_t)L.cnt * ((p->pop + 2 * n - 1) / (2 * n)); };
             while (sn > 16 && ctas(sn) < 2u * 296u) sn /= 2;
-            bool want = true;
-            if (const char *ov = getenv("VD_GA_SYNC")) want = atoi(ov) != 0;  /* 0: persistent kernels (A/B, tests) */
+            /* ga_step_kernel keeps the fitness and the elite flags in shared memory (5 B per
+               individual); populations beyond that stay on the persistent kernels, which
+               fail cleanly */
+            const unsigned step_bytes = 5u * (unsigned)p->pop + 16u;
+            bool want = step_bytes <= 200u * 1024u;
+            if (want && step_bytes > 48u * 1024u)
+                want = vdi::raise_smem_limit((const void *)vd::ga_step_kernel, step_bytes) == cudaSuccess;
+            if (const char *ov = getenv("VD_GA_SYNC")) want = want && atoi(ov) != 0;  /* 0: persistent kernels (A/B, tests) */
             cudaError_t e = cudaSuccess;
             for (int l : v)
                 L.s_bytes = std::max(L.s_bytes, vd::smem_layout(views[l].n_atoms, views[l].n_torsions, views[l].n_frag,
@@ -1249,7 +1255,7 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
 #ifdef VD_CHECKED
             VD_CK(cudaMemsetAsync(L.s_genes, 0xff, sizeof(double) * 2 * npop * L.s_gmax, ls));
 #endif
-            vd::ga_init_kernel<<<dim3((p->pop + 127) / 128, L.cnt), 128, 0, ls>>>(
+            vd::ga_init_kernel<<<dim3(L.cnt, (p->pop + 127) / 128), 128, 0, ls>>>(
                 d_views, d_order + L.off, P, seed, lig_index_base, L.s_genes, L.s_gmax);
             ++vdi::g_launches;
             VD_CK(cudaGetLastError());

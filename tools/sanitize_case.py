@@ -75,19 +75,22 @@ def main(out_path):
     batch = hostprep.TopologyBatch.synth(2, 0, 40)
     arrays = hostprep.prepare_batch(batch, grid.labels)
     lset = hostprep.ligand_set(arrays)
-    r = _run(grid, lset, 0, 40, GaConfig(population_size=64, generations=3,
-                                         translation_bounds=(spec.origin, spec.upper)),
-             0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
-    for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
-        out[f"batch_ga_{k}"] = v
-    # the same batch through the generation-synchronous path (bit-identical by design)
-    os.environ["VD_GA_SYNC"] = "1"
+    # the persistent kernels (one CTA per ligand, 4 / 8 subs with the role split) ...
+    os.environ["VD_GA_SYNC"] = "0"
     r = _run(grid, lset, 0, 40, GaConfig(population_size=64, generations=3,
                                          translation_bounds=(spec.origin, spec.upper)),
              0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
     del os.environ["VD_GA_SYNC"]
     for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
+        out[f"batch_ga_{k}"] = v
+    # ... and the same batch through the default generation-synchronous path (pop_score_kernel +
+    # ga_step_kernel; bit-identical to the persistent kernels by design)
+    r = _run(grid, lset, 0, 40, GaConfig(population_size=64, generations=3,
+                                         translation_bounds=(spec.origin, spec.upper)),
+             0, 0, _abi.MODE_FAST, 7 + int(batch.n_torsions.max()))
+    for k, v in zip(("bt", "be", "ba", "bg", "tr", "ne"), r):
         out[f"sync_ga_{k}"] = v
+        assert np.array_equal(np.asarray(v).view(np.uint8), np.asarray(out[f"batch_ga_{k}"]).view(np.uint8)), k
     # large ligands in a small batch: the team kernel (a ligand's population over 8 CTAs)
     b4 = hostprep.TopologyBatch.synth(4, 0, 6)
     l4 = hostprep.ligand_set(hostprep.prepare_batch(b4, grid.labels))
