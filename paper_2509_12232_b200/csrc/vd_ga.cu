@@ -2,9 +2,14 @@
  * vd_ga.cu -- the whole GA of vd/ga.py:180-235 on the device, for a batch of
  * ligands (vd/screening.py:165-244 semantics, ligand i keyed (seed, base+i)).
  *
+ * Two device paths, bit-identical to each other (vd_dock_batch picks per group of ligands):
+ *   generation-synchronous (fast mode, ligands up to 96 atoms): per generation one
+ *     pop_score_kernel launch over all (ligand, pose tile) CTAs and one ga_step_kernel
+ *     launch (one CTA per ligand); see the section of that name below
+ *   persistent (exact mode, larger ligands, VD_GA_SYNC=0): ga_kernel / ga_team_kernel.
  * Persistent CTAs pull ligands from an atomic work counter (host passes a
  * largest-first order), so ligands of very different sizes balance across
- * the 148 SMs.  One CTA runs one ligand's GA for all generations:
+ * the 148 SMs.  One CTA (or team of CTAs) runs one ligand's GA for all generations:
  *   score   thread-per-individual fused pose+inter+intra (vd_device.cuh)
  *   select  block arg-min for the generation best / elites (first index on ties)
  *   breed   thread-per-child tournament, two-point crossover, Gaussian
@@ -458,10 +463,10 @@ __global__ void __launch_bounds__(NPP *TPP) ga_team_kernel(GridView Gv, const Li
  *                     the batch's population buffer in global memory
  *   ga_step_kernel    one CTA per ligand: generation best, elites, children (the same
  *                     block_argmin / breed_child code and random streams as ga_kernel)
- * Same GA, same streams; the fast energies differ from ga_kernel's in the last bits (the role
- * split partitions the fp32 partial sums differently), each still a function of the
- * individual's genes alone.  Populations live at pop * gmax doubles per ligand slot,
- * individuals at stride G = 7 + T inside it (as in ga_kernel's buffers). */
+ * Same GA, same streams, and -- since ga_kernel runs a ligand's own sub count and the same role
+ * split -- the same energies: both paths are bit-identical (tests/test_gpu_ga.py), each energy
+ * a function of the individual's genes alone.  Populations live at pop * gmax doubles per
+ * ligand slot, individuals at stride G = 7 + T inside it (as in ga_kernel's buffers). */
 template <int NPP, int TPP, int LAY>
 __global__ void __launch_bounds__(NPP *TPP) pop_score_kernel(GridView G, const LigView *__restrict__ ligs,
                                                              const int *__restrict__ order,
