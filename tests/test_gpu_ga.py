@@ -298,6 +298,40 @@ def test_generation_synchronous_path_is_bit_identical_to_persistent_kernels(cuda
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
 
 
+def test_concurrent_host_threads_dock_batches_of_shared_shapes(cuda):
+    """Four host threads dock different slices of a cfg2 batch at once (the reference's
+    screen_batch worker pool does this, one ligand per call).  The generation-synchronous
+    path sets a per-function carveout before each of its launches and the slices share
+    kernel functions: results must equal the sequential ones byte for byte."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2509_12232_b200 import _abi, gridmaps, hostprep, synth
+    from paper_2509_12232_b200.ga import GaConfig, _run
+
+    spec = synth.config_grid_spec(2)
+    gset = gridmaps.build_grid_maps(synth.config_protein(2), spec, synth.CONFIGS[2].probe_types)
+    grid = cuda["fast"]._grid_for_set(gset)
+    batch = hostprep.TopologyBatch.synth(2, 0, 64)
+    lset = hostprep.ligand_set(hostprep.prepare_batch(batch, grid.labels))
+    ga = GaConfig(population_size=128, generations=12, translation_bounds=(spec.origin, spec.upper))
+    gmax = 7 + int(batch.n_torsions.max())
+    slices = [(0, 16), (16, 16), (32, 16), (48, 16), (5, 1), (40, 3)]
+
+    def work(sl):
+        return _run(grid, lset, sl[0], sl[1], ga, 11, sl[0], _abi.MODE_FAST, gmax)
+
+    want = [work(sl) for sl in slices]
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        got = list(ex.map(work, slices * 3))
+    for k, g in enumerate(got):
+        for x, y in zip(g, want[k % len(slices)]):
+            assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+    whole = _run(grid, lset, 0, 64, ga, 11, 0, _abi.MODE_FAST, gmax)
+    for sl, w in zip(slices, want):
+        assert np.array_equal(w[0], whole[0][sl[0]:sl[0] + sl[1]])   # batch-independent results
+        assert np.array_equal(w[3], whole[3][sl[0]:sl[0] + sl[1]])
+
+
 @pytest.mark.parametrize("team", ["2", "4", "8"])
 def test_team_split_ga_is_bit_identical(cuda, team, monkeypatch):
     """Large ligands in small batches split one ligand's population over a team of CTAs
