@@ -491,7 +491,7 @@ def screening_leg(args, rank, world, dist, dev):
                          else f"cfg2-distribution x{n}"),
             "gathered_records": int(rec.shape[0]), "gather_ms": round(1e3 * t_gather, 3),
             "host_prep_s_per_rank": round(prep_s, 3),
-            "timing": "CUDA events around vd_dock_batch (one persistent GA launch per atom-count bucket, buckets concurrent), max over ranks",
+            "timing": "CUDA events around vd_dock_batch (generation-synchronous GA: per generation one pop_score_kernel and one ga_step_kernel launch per launch-shape group of ligands, groups concurrent on streams; the exact leg: one persistent GA launch per atom-count bucket), max over ranks",
             "exact_mode": {"value": n / t_exact, "unit": "ligands/s", "ms": 1e3 * t_exact,
                            "note": "the same batch with reference-exact scoring (fp64 sums in "
                                    "the reference's lane-8 order, libm-equal exp): bit-identical "
