@@ -117,6 +117,9 @@ static __device__ void init_individual(const GaDev &P, int T, int i, uint64_t k0
     }
 }
 
+/* WIDE (ga_step_kernel, 64 registers to spare): the parent loads of four genes are issued
+   together; the persistent kernels keep one gene at a time (their register budget) */
+template <bool WIDE = false>
 static __device__ void breed_child(const GaDev &P, int G, const double *cur, const float *fit, int gen,
                             int c, uint64_t k0, uint64_t k1, double *child)
 {
@@ -139,6 +142,11 @@ static __device__ void breed_child(const GaDev &P, int G, const double *cur, con
     const int b = (int)vd_below(vd_words_get(&W, 2 * k + 2), (uint64_t)G + 1);
     const int c_lo = min(a, b), c_hi = max(a, b);
     bool mut_rot = false;
+    /* vd_u01(w) < rate  <=>  (w >> 11) < ceil(rate * 2^53): (w >> 11) is an integer below 2^53,
+       exact as a double, and scaling by 2^-53 is exact, so the integer compare decides every
+       word exactly as the fp64 one does (no u64 -> f64 conversion and fp64 multiply per gene);
+       WIDE only: in the cfg4 persistent kernel the change of register allocation cost 2% */
+    const uint64_t t_mut = !WIDE ? 0ull : P.mut_rate > 0.0 ? __double2ull_ru(fmin(P.mut_rate, 2.0) * 9007199254740992.0) : 0ull;
     /* genes in chunks of 32: first the crossover copy (+0.0, as child + where(mut, z*sigma, 0))
        and the mutation mask, then the normals for the set bits only, so a warp runs the
        normal sampler max-over-lanes(mutations) times rather than once per gene with any
@@ -146,10 +154,28 @@ static __device__ void breed_child(const GaDev &P, int G, const double *cur, con
     for (int g0 = 0; g0 < G; g0 += 32) {
         const int g1 = min(G, g0 + 32);
         uint32_t mask = 0;
-        for (int g = g0; g < g1; ++g) {
-            const double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
-            if (vd_u01(vd_words_get(&W, 2 * k + 3 + g)) < P.mut_rate) mask |= 1u << (g - g0);
-            child[g] = __dadd_rn(v, 0.0);
+        if (WIDE) {
+            /* four genes at a time: their parent loads are issued together, before the flags'
+               Philox blocks (one gene at a time, the load latency of every gene was exposed:
+               22% of ga_step_kernel's stall samples sat on the copy below) */
+            for (int g = g0; g < g1; g += 4) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (g + u < g1) v[u] = ((do_cx && g + u >= c_lo && g + u < c_hi) ? p2 : p1)[g + u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (g + u < g1) {
+                        if ((vd_words_get(&W, 2 * k + 3 + g + u) >> 11) < t_mut) mask |= 1u << (g + u - g0);
+                        child[g + u] = __dadd_rn(v[u], 0.0);
+                    }
+            }
+        } else {
+            for (int g = g0; g < g1; ++g) {
+                const double v = (do_cx && g >= c_lo && g < c_hi) ? p2[g] : p1[g];
+                if (vd_u01(vd_words_get(&W, 2 * k + 3 + g)) < P.mut_rate) mask |= 1u << (g - g0);
+                child[g] = __dadd_rn(v, 0.0);
+            }
         }
         while (mask) {
             const int g = g0 + __ffs(mask) - 1;
@@ -803,7 +829,7 @@ __global__ void __launch_bounds__(256, 4) ga_step_kernel(const LigView *__restri
         __syncthreads();
     }
     for (int c = threadIdx.x; c < pop - P.elitism; c += B)
-        breed_child(P, G, cur, fit, gen, c, k0, k1, nxt + (size_t)(P.elitism + c) * G);
+        breed_child<true>(P, G, cur, fit, gen, c, k0, k1, nxt + (size_t)(P.elitism + c) * G);
 }
 
 cudaError_t launch_ga(bool exact, int npp, int tpp, const GridView &Gv, const LigView *d_ligs,
