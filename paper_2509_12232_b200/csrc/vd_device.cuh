@@ -970,6 +970,27 @@ __device__ __forceinline__ void stage_resident(const LigView &L, const PairTile 
     if (T.resident) stage_pairs<EXACT, NPP>(L, T, 0, L.n_pairs);
 }
 
+/* FAST resident lists, staged asynchronously: the records are raw copies of the global arrays,
+ * so a CTA can start its pose stage (which needs only the topology) while cp.async fills the
+ * pair tile; the caller waits (cp_async_wait_all) before the barrier that ends the pose stage.
+ * (Staged synchronously, the prologue barrier held 6.5% of pop_score_kernel's stall samples:
+ * a 32 x 8 CTA loads ~30 KB of records for 64 poses.)  The checked build stages synchronously,
+ * with the per-record checks of stage_pairs. */
+template <int NPP>
+__device__ __forceinline__ void stage_resident_async(const LigView &L, const PairTile &T)
+{
+#ifdef VD_CHECKED
+    stage_resident<false, NPP>(L, T);
+#else
+    if (!T.resident) return;
+    for (int k = threadIdx.x; k < L.n_pairs; k += blockDim.x) {
+        cp_async16(T.coef + k, L.fcoef + k);
+        cp_async8(T.off + k, L.fij + k);
+    }
+    cp_async_commit();
+#endif
+}
+
 template <int NPP>
 __device__ __forceinline__ void exact_pair(const float2 *S, const PairTile &T, int k, float cut2,
                                            double &acc0, double &acc1)

@@ -515,14 +515,15 @@ __global__ void __launch_bounds__(NPP *TPP) pop_score_kernel(GridView G, const L
     const PairTile T = pair_tile(smem, lay);
     const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2,
                                      lay.topo_tors, lay.topo_frag);
-    stage_resident<false, NPP>(L, T);
+    stage_resident_async<NPP>(L, T);  /* lands during the pose stage */
     __syncthreads();
     const int Gn = 7 + L.n_torsions;
     const int i0 = (tile * NPP + pp) * 2, i1 = i0 + 1;
     const double *gb = genes + (size_t)slot * pop * gmax;
     build_pose2<NPP, TPP>(L, gb + (size_t)min(i0, pop - 1) * Gn, gb + (size_t)min(i1, pop - 1) * Gn, S,
                           sub, reinterpret_cast<float *>(smem + lay.scratch) + pp, G.one);
-    if (TPP > 1) __syncthreads();
+    cp_async_wait_all();  /* this thread's share of the pair records */
+    __syncthreads();
     double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
     energy2<false, NPP, TPP, false, ga_split(TPP), LAY>(L, G, S, T, sub, e0, e1, a0, a1,
                                                reinterpret_cast<double *>(smem + lay.red), pp, kGaSplitR);

@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
     const PairTile T = pair_tile(smem, lay);
     const LigView L = stage_topology(Lg, smem, lay.topo_atom, lay.topo_atom2, lay.topo_tors,
                                      lay.topo_frag);
-    stage_resident<EXACT, NPP>(L, T);
+    if (EXACT) stage_resident<EXACT, NPP>(L, T);
+    else stage_resident_async<NPP>(L, T);  /* lands during the pose stage */
     __syncthreads();
 #if VD_SCORE_PERSIST
     const int64_t n_tiles = (P + 2 * NPP - 1) / (2 * NPP);
@@ -72,15 +73,15 @@ __global__ void __launch_bounds__(NPP *TPP) score_kernel(GridView G, LigView Lg,
         if (genes) {
             build_pose2<NPP, TPP>(L, genes + q0 * ngenes, genes + q1 * ngenes, S, sub,
                                   reinterpret_cast<float *>(smem + lay.scratch) + pp, G.one);
-            if (TPP > 1) __syncthreads();
         } else {
             const int n = L.n_atoms;
             const float *s0 = poses + q0 * 3 * n, *s1 = poses + q1 * 3 * n;
             for (int i = sub; i < n; i += TPP)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) VD_S2(i, c) = f2(s0[c * n + i], s1[c * n + i]);
-            if (TPP > 1) __syncthreads();
         }
+        if (!EXACT) cp_async_wait_all();  /* this thread's share of the pair records */
+        if (TPP > 1 || !EXACT) __syncthreads();
         double e0 = 0.0, e1 = 0.0, a0 = 0.0, a1 = 0.0;
 #ifndef VD_TEST_STAGE
         energy2<EXACT, NPP, TPP, VD_SCORE_PIPE != 0, VD_SCORE_SPLIT != 0, LAY, VD_INTER_FLAT != 0>(
