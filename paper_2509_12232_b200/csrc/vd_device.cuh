@@ -973,9 +973,9 @@ __device__ __forceinline__ void stage_resident(const LigView &L, const PairTile 
 /* FAST resident lists, staged asynchronously: the records are raw copies of the global arrays,
  * so a CTA can start its pose stage (which needs only the topology) while cp.async fills the
  * pair tile; the caller waits (cp_async_wait_all) before the barrier that ends the pose stage.
- * (Staged synchronously, the prologue barrier held 6.5% of pop_score_kernel's stall samples:
- * a 32 x 8 CTA loads ~30 KB of records for 64 poses.)  The checked build stages synchronously,
- * with the per-record checks of stage_pairs. */
+ * (Staged synchronously, a 32 x 8 CTA waited for ~30 KB of records before the pose stage of
+ * its 64 poses: cfg2 screen 960 -> 941 ms.)  The checked build stages synchronously, with the
+ * per-record checks of stage_pairs. */
 template <int NPP>
 __device__ __forceinline__ void stage_resident_async(const LigView &L, const PairTile &T)
 {

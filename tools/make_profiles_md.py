@@ -64,8 +64,7 @@ pop = body("r2c_pop_score.md").replace("# r2c pop_score", "# r2 (final) pop_scor
 pop += "\n## per-stage stall samples\n```\n" + body("r2c_pop_score_stalls.txt") + "```\n```\n" + body("r2c_pop_score_regions.txt") + "```\n" + NOTE
 pop += ("\nThe barrier share is the wait at the role split's join plus the pose chain: a GA population sits in the box, every atom "
         "gathers, and the pair subs wait for the gather subs or vice versa; a sweep of the balance constant (VD_GA_SPLIT_R 13..46) "
-        "left 26 the best (cfg2 screen 977 ms; 980-1021 ms for the others).  Before the pair records were staged with cp.async "
-        "during the pose stage, the prologue barrier alone held 6.5% of the samples (22.1% barrier in total).\n")
+        "left 26 the best (cfg2 screen 977 ms; 980-1021 ms for the others).\n")
 (out / "r2c_pop_score.md").write_text(pop)
 step_md = body("r2c_ga_step.md").replace("# r2c ga_step", "# r2 (final) ga_step_kernel (64 registers, 4 CTAs/SM, four genes' parent loads issued together)")
 (out / "r2c_ga_step.md").write_text(step_md)
