@@ -1,8 +1,9 @@
 """Memory and race checking without compute-sanitizer (closed on this pool).
 
-tools/sanitize_case.py drives every hot kernel shape (score TPP 1/4/8 with resident and
-streamed pair tiles and the role split, pose TPP 1/4/8, GA fast packed / plain / exact and
-concurrent bucket launches, grid build, MUGD transpose) twice, in separate processes:
+tools/sanitize_case.py drives every hot kernel shape (score TPP 1/4/8/16 with resident and
+streamed pair tiles and the role split, pose TPP 1/4/8/16, GA fast packed / plain / exact, a
+batch through the persistent kernels and through the generation-synchronous path, the team
+kernel, grid build, MUGD transpose) twice, in separate processes:
   * with the production library, and
   * with libvdb200_checked.so (-DVD_CHECKED): device bounds and invariant checks on map
     indices, atom / fragment / pair indices, gather cells, GA individual indices and the
