@@ -34,7 +34,7 @@
 #include "vd_internal.h"
 #include "vd_rng.h"
 
-/* Build parts (as in vd_score.cu): VD_PART undefined = one unit (the checked build);
+/* Build parts (as in vd_score.cu): VD_PART undefined = one unit;
  * 0 = dispatch, probes and the C entry points; 1..5 = the GA kernels of TPP 1, 2, 4, 8, 16. */
 #ifndef VD_PART
 #define VD_PART -1
@@ -908,7 +908,9 @@ void chk_selftest_ga()
     vd::chk_selftest_ga_kernel<<<1, 32>>>(1);
 }
 
-unsigned chk_flags_ga(bool clear)
+/* the check-flag word is per translation unit: every build part reads its own, part 0 (or
+   the single unit) ORs them */
+static unsigned chk_read_own(bool clear)
 {
 #ifdef VD_CHECKED
     unsigned v = 0;
@@ -922,6 +924,19 @@ unsigned chk_flags_ga(bool clear)
     (void)clear;
     return 0;
 #endif
+}
+#if VD_PART == 0
+unsigned chk_flags_ga_p1(bool), chk_flags_ga_p2(bool), chk_flags_ga_p3(bool), chk_flags_ga_p4(bool),
+    chk_flags_ga_p5(bool);
+#endif
+unsigned chk_flags_ga(bool clear)
+{
+    unsigned v = chk_read_own(clear);
+#if VD_PART == 0
+    v |= chk_flags_ga_p1(clear) | chk_flags_ga_p2(clear) | chk_flags_ga_p3(clear) |
+         chk_flags_ga_p4(clear) | chk_flags_ga_p5(clear);
+#endif
+    return v;
 }
 }  // namespace vdi
 
@@ -1363,4 +1378,25 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
 }
 #else
 }  // namespace vd
+
+namespace vdi {
+#define VD_CAT2(a, b) a##b
+#define VD_CAT(a, b) VD_CAT2(a, b)
+/* this part's check-flag word (see chk_flags_ga in part 0) */
+unsigned VD_CAT(chk_flags_ga_p, VD_PART)(bool clear)
+{
+#ifdef VD_CHECKED
+    unsigned v = 0;
+    cudaMemcpyFromSymbol(&v, vd::g_vd_chk_flags, sizeof v);
+    if (clear) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(vd::g_vd_chk_flags, &z, sizeof z);
+    }
+    return v;
+#else
+    (void)clear;
+    return 0;
+#endif
+}
+}  // namespace vdi
 #endif  /* VD_PART <= 0 */

@@ -17,7 +17,7 @@
 
 /* Build parts: the 33 score_kernel instantiations are compiled as five translation units
  * (one per TPP) plus the dispatch, so that `make -j` builds them in parallel:
- *   VD_PART undefined  everything in this one unit (the checked build)
+ *   VD_PART undefined  everything in this one unit
  *   VD_PART 0          dispatch, pose kernels, shape choice; launch_t<> declared extern
  *   VD_PART 1..5       launch_t<*, *, TPP> for TPP = 1, 2, 4, 8, 16 */
 #ifndef VD_PART
@@ -404,7 +404,45 @@ void chk_selftest_score()
     vd::chk_selftest_score_kernel<<<1, 32>>>(1);
 }
 
+/* the check-flag word is per translation unit: every build part reads its own, part 0 (or
+   the single unit) ORs them */
+static unsigned chk_read_own(bool clear)
+{
+#ifdef VD_CHECKED
+    unsigned v = 0;
+    cudaMemcpyFromSymbol(&v, vd::g_vd_chk_flags, sizeof v);
+    if (clear) {
+        const unsigned z = 0;
+        cudaMemcpyToSymbol(vd::g_vd_chk_flags, &z, sizeof z);
+    }
+    return v;
+#else
+    (void)clear;
+    return 0;
+#endif
+}
+#if VD_PART == 0
+unsigned chk_flags_score_p1(bool), chk_flags_score_p2(bool), chk_flags_score_p3(bool), chk_flags_score_p4(bool),
+    chk_flags_score_p5(bool);
+#endif
 unsigned chk_flags_score(bool clear)
+{
+    unsigned v = chk_read_own(clear);
+#if VD_PART == 0
+    v |= chk_flags_score_p1(clear) | chk_flags_score_p2(clear) | chk_flags_score_p3(clear) |
+         chk_flags_score_p4(clear) | chk_flags_score_p5(clear);
+#endif
+    return v;
+}
+}  // namespace vdi
+#else
+}  // namespace vd
+
+namespace vdi {
+#define VD_CAT2(a, b) a##b
+#define VD_CAT(a, b) VD_CAT2(a, b)
+/* this part's check-flag word (see chk_flags_score in part 0) */
+unsigned VD_CAT(chk_flags_score_p, VD_PART)(bool clear)
 {
 #ifdef VD_CHECKED
     unsigned v = 0;
@@ -420,6 +458,4 @@ unsigned chk_flags_score(bool clear)
 #endif
 }
 }  // namespace vdi
-#else
-}  // namespace vd
 #endif  /* VD_PART <= 0 */
