@@ -903,9 +903,15 @@ __global__ void chk_selftest_ga_kernel(int bad) { VD_CHK(bad == 0, VD_SITE_POP);
 }  // namespace vd
 
 namespace vdi {
+#if VD_PART == 0
+void chk_selftest_ga_part();  /* raises a flag in another build part's word */
+#endif
 void chk_selftest_ga()
 {
     vd::chk_selftest_ga_kernel<<<1, 32>>>(1);
+#if VD_PART == 0
+    chk_selftest_ga_part();
+#endif
 }
 
 /* the check-flag word is per translation unit: every build part reads its own, part 0 (or
@@ -1382,6 +1388,18 @@ extern "C" int vd_dock_batch(const vd_grid *g, const vd_ligands *s, int first, i
 namespace vdi {
 #define VD_CAT2(a, b) a##b
 #define VD_CAT(a, b) VD_CAT2(a, b)
+#if VD_PART == 3
+}  // namespace vdi
+namespace vd {
+__global__ void chk_selftest_ga_part_kernel(int bad) { VD_CHK(bad == 0, VD_SITE_CELL); }
+}  // namespace vd
+namespace vdi {
+/* self-test of the per-part flag words: raise a flag in THIS part (read back through part 0) */
+void chk_selftest_ga_part()
+{
+    vd::chk_selftest_ga_part_kernel<<<1, 32>>>(1);
+}
+#endif
 /* this part's check-flag word (see chk_flags_ga in part 0) */
 unsigned VD_CAT(chk_flags_ga_p, VD_PART)(bool clear)
 {

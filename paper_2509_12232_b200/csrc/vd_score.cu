@@ -399,9 +399,15 @@ __global__ void chk_selftest_score_kernel(int bad) { VD_CHK(bad == 0, VD_SITE_TI
 }  // namespace vd
 
 namespace vdi {
+#if VD_PART == 0
+void chk_selftest_score_part();  /* raises a flag in another build part's word */
+#endif
 void chk_selftest_score()
 {
     vd::chk_selftest_score_kernel<<<1, 32>>>(1);
+#if VD_PART == 0
+    chk_selftest_score_part();
+#endif
 }
 
 /* the check-flag word is per translation unit: every build part reads its own, part 0 (or
@@ -441,6 +447,18 @@ unsigned chk_flags_score(bool clear)
 namespace vdi {
 #define VD_CAT2(a, b) a##b
 #define VD_CAT(a, b) VD_CAT2(a, b)
+#if VD_PART == 3
+}  // namespace vdi
+namespace vd {
+__global__ void chk_selftest_score_part_kernel(int bad) { VD_CHK(bad == 0, VD_SITE_SMEM); }
+}  // namespace vd
+namespace vdi {
+/* self-test of the per-part flag words: raise a flag in THIS part (read back through part 0) */
+void chk_selftest_score_part()
+{
+    vd::chk_selftest_score_part_kernel<<<1, 32>>>(1);
+}
+#endif
 /* this part's check-flag word (see chk_flags_score in part 0) */
 unsigned VD_CAT(chk_flags_score_p, VD_PART)(bool clear)
 {
