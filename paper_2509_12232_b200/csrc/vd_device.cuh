@@ -904,6 +904,9 @@ constexpr float kSplitR = VD_SPLIT_R;
 #ifndef VD_ROLE_NI8
 #define VD_ROLE_NI8 4   /* gather subs per 8 subs in the role-split energy stage */
 #endif
+#ifndef VD_ROLE_NI_T8
+#define VD_ROLE_NI_T8 4   /* gather subs of the 8-sub shapes (3 / 5 measured: see DESIGN) */
+#endif
 #ifndef VD_INTRA_ROWS
 #define VD_INTRA_ROWS 1
 #endif
@@ -1207,7 +1210,7 @@ __device__ __forceinline__ void energy2(const LigView &L, const GridView &G, con
        one CTA instead of only across CTAs.  Resident pair lists only (the streamed path has
        CTA barriers).  cfg1: 1.603 vs 1.683 ms (NI = 2 of 4); NI = 1 or 3 of 4: 2.23 / 1.76 ms.
        The GA does not split (7,022 vs 8,621 ligands/s): it pipelines its gathers instead. */
-    constexpr int NI = TPP * VD_ROLE_NI8 / 8 > 0 ? TPP * VD_ROLE_NI8 / 8 : 1;
+    constexpr int NI = TPP == 8 ? VD_ROLE_NI_T8 : (TPP * VD_ROLE_NI8 / 8 > 0 ? TPP * VD_ROLE_NI8 / 8 : 1);
     constexpr int NA = TPP - NI > 0 ? TPP - NI : 1;
     VD_JITTER(100);
     if (SPLIT && !EXACT && TPP >= 4 && NI < TPP && T.resident) {
